@@ -1,0 +1,254 @@
+/*
+ * spidgpu.h -- C ABI of the B200-native SPID compression path.
+ *
+ * This is the drop-in boundary for the reference's per-subdomain compressor
+ * (namespace spid in /root/reference/proj/include/spid). The reference
+ * exposes header-level C++ with value semantics and exceptions; a C ABI
+ * replaces those with caller-owned buffers and status codes
+ * (spidgpu_status.h), whose names are the reference's spid::Error names.
+ *
+ * Conventions (all entry points):
+ *   - matrices are column-major fp64, exactly the reference DenseMatrix
+ *     layout ((i,j) at data[j*ld+i], proj/include/spid/dense_matrix.hpp:33-34);
+ *   - a batch of S subdomains is S matrices at a fixed element stride;
+ *   - skeleton indices are int64 in pivot-selection order and coefficient
+ *     matrices are kcap x n (ld kcap) in SOURCE column order with an exact
+ *     identity block C(:, I) = I  (proj/src/id.cpp:9-28);
+ *   - "_batched" calls take DEVICE pointers and a cudaStream_t (as void*),
+ *     are asynchronous, allocate nothing on the hot path, and report
+ *     per-subdomain failures in an int32 status array;
+ *   - the non-batched calls take HOST pointers and mirror the reference
+ *     functions one for one (synchronous, like the reference);
+ *   - there is no CPU fallback: without a usable sm_100 device every call
+ *     returns SPID_NO_DEVICE / SPID_CUDA_ERROR.
+ *
+ * One handle per host thread (or stream): handles are independent, which
+ * keeps the ABI as reentrant as the reference's pure functions
+ * (SURVEY 8(b) "Threading").
+ */
+#ifndef SPIDGPU_H
+#define SPIDGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "spidgpu_status.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPIDGPU_ABI_VERSION 1
+
+typedef struct spidgpu_context* spidgpu_handle;
+
+/* ---- rank rule: replaces spid::RankRule (proj/include/spid/qr.hpp:12-37) ---- */
+#define SPIDGPU_RULE_FIXED 0   /* RankRule::fixed(k)                         */
+#define SPIDGPU_RULE_TOL 1     /* RankRule::tolerance(tol)                   */
+#define SPIDGPU_RULE_BLOCKED 2 /* BASELINE cfg4: rank grows in steps of kstep
+                                  up to k until residual_fro/||Y||_F <= tol   */
+typedef struct spidgpu_rank_rule {
+    int32_t mode;
+    int32_t at_most; /* 1 = column_id_at_most semantics (qr.cpp:22-25): k is
+                        capped at min(k, rows, cols) and a collapse stops
+                        quietly instead of raising RankUnreachable            */
+    int64_t k;       /* FIXED: target rank; BLOCKED: kmax                       */
+    int64_t kstep;   /* BLOCKED only                                           */
+    double tol;      /* TOL / BLOCKED                                          */
+} spidgpu_rank_rule;
+
+/* ---- sketch operator Omega (BASELINE north_star: Gaussian, ell = k + p rows) ---- */
+#define SPIDGPU_OMEGA_EXPLICIT 0 /* oracle mode: Omega_s given, ell x m, ld ldo   */
+#define SPIDGPU_OMEGA_PHILOX 1   /* performance mode: generated in-kernel        */
+typedef struct spidgpu_omega {
+    int32_t mode;
+    int32_t reserved;
+    const double* omega;     /* EXPLICIT: device (batched) or host (host API) */
+    int64_t ldo;             /* EXPLICIT: leading dimension (>= ell)           */
+    int64_t stride;          /* EXPLICIT: elements between Omega_s, Omega_s+1  */
+    uint64_t seed;           /* PHILOX: key                                    */
+    int64_t subdomain_base;  /* PHILOX: global id of batch element 0           */
+} spidgpu_omega;
+
+/* ---- lifecycle / diagnostics ---- */
+int spidgpu_create(int device, spidgpu_handle* out);
+int spidgpu_destroy(spidgpu_handle h);
+/* Reference error name for a status code ("ZeroMatrix", ...); "Ok" for 0. */
+const char* spidgpu_status_name(int status);
+/* Human-readable message of the handle's last failure ("" if none). */
+const char* spidgpu_last_error(spidgpu_handle h);
+int spidgpu_abi_version(void);
+/* Kernel launches issued through this handle since creation (instrumentation). */
+int64_t spidgpu_launch_count(spidgpu_handle h);
+
+/* =====================================================================
+ * Batched device API (the hot path). Subdomain s of a batch lives at
+ * A + s*strideA (m x n, ld lda). All outputs are caller-allocated device
+ * buffers sized by kcap; stream may be NULL (legacy default stream).
+ * ===================================================================== */
+
+/* Y_s = Omega_s * A_s  (ell x n, ld ldy, stride strideY). Replaces the
+ * reference sketch entry subsample()/subsample_column() (proj/src/grid.cpp:
+ * 136-150, used by spid() at proj/src/id.cpp:75-80) with the Gaussian sketch
+ * of the north star; restated by matmul (proj/src/dense_matrix.cpp:38-53).
+ * FP64 DMMA, A staged by TMA, deterministic split-K. */
+int spidgpu_sketch_batched(spidgpu_handle h, const double* A, int64_t m, int64_t n, int64_t lda,
+                           int64_t strideA, int64_t batch, int64_t ell, const spidgpu_omega* omega,
+                           double* Y, int64_t ldy, int64_t strideY, void* stream);
+
+/* Materialise the Omega_s that SPIDGPU_OMEGA_PHILOX uses (ell x m, ld ldo) so
+ * an oracle can be fed the same bits. */
+int spidgpu_philox_omega(spidgpu_handle h, uint64_t seed, int64_t subdomain, int64_t ell,
+                         int64_t m, double* omega, int64_t ldo, void* stream);
+
+/* Column ID of each Y_s (rows x n): greedy CPQR + coefficient solve, one
+ * subdomain per CTA. Replaces column_id / column_id_at_most
+ * (proj/src/id.cpp:40-52) -> pivoted_mgs_qr (proj/src/qr.cpp:18-124) ->
+ * build_coeffs + solve_upper_triangular (id.cpp:9-28, qr.cpp:128-151).
+ * Bit-identical to the reference for identical Y (same summation order, no
+ * FMA contraction). Outputs per subdomain s:
+ *   indices[s*kcap ..]     selection-order skeleton indices (rank entries)
+ *   C[s*strideC ..]        kcap x n, ld kcap (rows >= rank untouched)
+ *   rank[s], residual_fro[s], status[s]
+ * Optional (NULL to skip): pivots (n per subdomain, full permutation),
+ *   R (kcap x n per subdomain, ld kcap, pivoted column order as
+ *   QrFactorization::r_mat), Q (rows x kcap per subdomain, ld rows). */
+int spidgpu_cpqr_id_batched(spidgpu_handle h, const double* Y, int64_t rows, int64_t n,
+                            int64_t ldy, int64_t strideY, int64_t batch,
+                            const spidgpu_rank_rule* rule, int64_t kcap, int64_t* indices,
+                            double* C, int64_t strideC, int64_t* rank, double* residual_fro,
+                            int32_t* status, int64_t* pivots, double* R, double* Q, void* stream);
+
+/* skel_s(:, t) = A_s(:, indices_s[t]) for t < rank[s]: select_columns
+ * (proj/src/dense_matrix.cpp:71-81) -- the fine skeleton of sub_id
+ * (proj/src/id.cpp:57-58). */
+int spidgpu_gather_batched(spidgpu_handle h, const double* A, int64_t m, int64_t n, int64_t lda,
+                           int64_t strideA, int64_t batch, const int64_t* indices, int64_t kcap,
+                           const int64_t* rank, double* skel, int64_t ldskel, int64_t strideS,
+                           void* stream);
+
+/* B_s = A_s(J, :) for a strictly increasing row set J (nrows entries):
+ * subsample (proj/src/grid.cpp:136-140). Output ld ldb, stride strideB. */
+int spidgpu_row_gather_batched(spidgpu_handle h, const double* A, int64_t m, int64_t n,
+                               int64_t lda, int64_t strideA, int64_t batch, const int64_t* rows,
+                               int64_t nrows, double* B, int64_t ldb, int64_t strideB,
+                               void* stream);
+
+/* Exact verification terms per subdomain: err2[s] = ||A_s - skel_s C_s||_F^2,
+ * ref2[s] = ||A_s||_F^2 (reconstruct + rel_frob_error, proj/src/id.cpp:85-90,
+ * proj/src/metrics.cpp:14-21). FP64 DMMA, deterministic reduction. */
+int spidgpu_verify_batched(spidgpu_handle h, const double* A, int64_t m, int64_t n, int64_t lda,
+                           int64_t strideA, int64_t batch, const double* skel, int64_t ldskel,
+                           int64_t strideS, const double* C, int64_t kcap, int64_t strideC,
+                           const int64_t* rank, double* err2, double* ref2, void* stream);
+
+/* out_s = skel_s * C_s (m x n, ld ldo): reconstruct (proj/src/id.cpp:85-90). */
+int spidgpu_reconstruct_batched(spidgpu_handle h, const double* skel, int64_t m, int64_t ldskel,
+                                int64_t strideS, const double* C, int64_t kcap, int64_t strideC,
+                                const int64_t* rank, int64_t n, int64_t batch, double* out,
+                                int64_t ldo, int64_t strideO, void* stream);
+
+/* The fused compress driver: sketch -> CPQR/coefficients -> skeleton gather
+ * for a batch of subdomains (the CLI batch loop, proj/tools/spid_cli.cpp:
+ * 220-231, with sub_id's fine skeleton). skel may be NULL (no gather); Y may
+ * be NULL (sketch kept in the handle's workspace). */
+int spidgpu_compress_batched(spidgpu_handle h, const double* A, int64_t m, int64_t n, int64_t lda,
+                             int64_t strideA, int64_t batch, int64_t ell,
+                             const spidgpu_omega* omega, const spidgpu_rank_rule* rule,
+                             int64_t kcap, int64_t* indices, double* C, int64_t* rank,
+                             double* residual_fro, int32_t* status, double* skel, double* Y,
+                             void* stream);
+
+/* =====================================================================
+ * Host-buffer API: one call per reference function (synchronous).
+ * ===================================================================== */
+
+/* spid::column_id / column_id_at_most (proj/src/id.cpp:40-52).
+ * coeffs: kcap x n (ld kcap); skeleton: m x kcap (ld m), may be NULL. */
+int spidgpu_column_id(spidgpu_handle h, const double* a, int64_t m, int64_t n,
+                      const spidgpu_rank_rule* rule, int64_t kcap, int64_t* indices,
+                      double* coeffs, double* skeleton, int64_t* rank, double* residual_fro);
+
+/* spid::pivoted_mgs_qr / _at_most (proj/src/qr.cpp:18-25) with the full
+ * QrFactorization: q (m x kcap, ld m), r (kcap x n, ld kcap), pivots (n). */
+int spidgpu_qr(spidgpu_handle h, const double* a, int64_t m, int64_t n,
+               const spidgpu_rank_rule* rule, int64_t kcap, double* q, double* r, int64_t* pivots,
+               int64_t* rank, double* residual_fro);
+
+/* spid::sub_id (proj/src/id.cpp:54-60) with the row set J of the spec given
+ * explicitly (SubsampleSpec::row_indices, proj/src/grid.cpp:108-130). */
+int spidgpu_sub_id(spidgpu_handle h, const double* a, int64_t m, int64_t n, const int64_t* rows,
+                   int64_t nrows, const spidgpu_rank_rule* rule, int64_t kcap, int64_t* indices,
+                   double* coeffs, double* skeleton, int64_t* rank, double* residual_fro);
+
+/* Gaussian-sketch SubID of one subdomain: Y = Omega A, column_id(Y), fine
+ * skeleton A(:, I). omega->omega (EXPLICIT) is a HOST pointer here. y (ell x
+ * n) may be NULL. */
+int spidgpu_sketch_id(spidgpu_handle h, const double* a, int64_t m, int64_t n, int64_t ell,
+                      const spidgpu_omega* omega, const spidgpu_rank_rule* rule, int64_t kcap,
+                      double* y, int64_t* indices, double* coeffs, double* skeleton,
+                      int64_t* rank, double* residual_fro);
+
+/* spid::reconstruct / pyspid.reconstruct (proj/src/id.cpp:85-90): out = skel * coeffs
+ * (skel m x k, coeffs k x n, out m x n). */
+int spidgpu_reconstruct(spidgpu_handle h, const double* skeleton, int64_t m, int64_t k,
+                        const double* coeffs, int64_t n, double* out);
+
+/* spid::rel_frob_error (proj/src/metrics.cpp:14-21), computed on the device. */
+int spidgpu_rel_frob_error(spidgpu_handle h, const double* exact, const double* approx, int64_t m,
+                           int64_t n, double* out);
+
+/* spid::compression_factor (proj/src/metrics.cpp:5-12): pure arithmetic. */
+int spidgpu_compression_factor(int64_t m, int64_t n, int64_t stored, double* out);
+
+/* End-to-end batched compression from HOST buffers: the reference-facing
+ * batch call (one spid() per block, proj/tools/spid_cli.cpp:220-231) with the
+ * host<->device traffic inside. Subdomain s of A is at a + s*m*n (m x n, ld m).
+ * Streams subdomains through device memory in groups of `group` with copy /
+ * compute overlap. Outputs (host): indices (batch x kcap), coeffs (batch x
+ * kcap x n), skel (batch x m x kcap, may be NULL), rank, residual_fro, status.
+ * If err2/ref2 are non-NULL the verify pass runs too. */
+int spidgpu_compress_host(spidgpu_handle h, const double* a, int64_t m, int64_t n, int64_t batch,
+                          int64_t ell, const spidgpu_omega* omega, const spidgpu_rank_rule* rule,
+                          int64_t kcap, int64_t group, int64_t* indices, double* coeffs,
+                          double* skel, int64_t* rank, double* residual_fro, int32_t* status,
+                          double* err2, double* ref2);
+
+/* =====================================================================
+ * Synthetic input fields (bench/tests only; not a reference interface).
+ * Taylor-Green-vortex families of BASELINE.json configs 1-5, generated in
+ * place on the device for a batch of subdomains of a periodic N^3 grid split
+ * into blocks of b^3 (make_block_domains order, proj/src/blocking.cpp:31-98),
+ * rows QoI-major (row = q*b^3 + local point, axis 0 fastest).
+ * ===================================================================== */
+#define SPIDGPU_FIELD_TGV4 0      /* cfg1: u, v, w=0, p (incompressible TGV)  */
+#define SPIDGPU_FIELD_TGV5 1      /* cfg2: rho, u, v, w, E (compressible)     */
+#define SPIDGPU_FIELD_MULTIMODE 2 /* cfg3/4/5: TGV5 + random Fourier modes    */
+typedef struct spidgpu_field_spec {
+    int32_t kind;
+    int32_t n_modes;        /* MULTIMODE: number of extra Fourier modes      */
+    int64_t grid;           /* N (points per axis of the whole grid)         */
+    int64_t block;          /* b (points per axis of one subdomain)          */
+    int64_t snapshots;      /* n                                             */
+    double t_end;           /* snapshots uniform in [0, t_end] (inclusive)   */
+    double nu;              /* viscosity                                     */
+    double noise_sigma;     /* additive N(0, sigma^2) noise                  */
+    double kappa_max;       /* MULTIMODE: |kappa| bound                      */
+    double mode_amp;        /* MULTIMODE: amplitude scale (x |kappa|^-5/3)   */
+    uint64_t seed;          /* modes and noise                               */
+    int64_t heavy_modes;    /* cfg4: extra high-wavenumber modes on "heavy"  */
+    double heavy_kmin;      /* cfg4: |kappa| lower bound of heavy modes      */
+} spidgpu_field_spec;
+
+/* Fill batch subdomains [first, first+batch) (global block ids) into A
+ * (m x n per subdomain, ld lda, stride strideA). For cfg4, subdomains with
+ * is_heavy[s] != 0 (host array, may be NULL) get the extra modes. */
+int spidgpu_field_generate(spidgpu_handle h, const spidgpu_field_spec* spec, int64_t first,
+                           int64_t batch, const uint8_t* is_heavy, double* A, int64_t lda,
+                           int64_t strideA, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -111,6 +111,8 @@ class _Port:
         L = C.CDLL(path)
         L.orc_seeded_sym.argtypes = [C.c_uint64, _D, _sz]
         L.orc_gaussian.argtypes = [C.c_uint64, _D, _sz]
+        L.orc_splitmix_next.argtypes = [C.POINTER(C.c_uint64)]
+        L.orc_splitmix_next.restype = C.c_uint64
         L.orc_matmul.argtypes = [_D, _sz, _sz, _D, _sz, _D]
         L.orc_frobenius.argtypes = [_D, _sz]
         L.orc_frobenius.restype = C.c_double
@@ -136,6 +138,13 @@ class _Port:
         out = np.empty((m, n), dtype=np.float64, order="F")
         self.lib.orc_seeded_sym(seed, _dp(out), m * n)
         return out
+
+    def splitmix_next(self, state: list) -> int:
+        """SplitMix64::next_u64 on a one-element list holding the state."""
+        st = C.c_uint64(state[0])
+        v = self.lib.orc_splitmix_next(C.byref(st))
+        state[0] = st.value
+        return int(v)
 
     def seeded_vector(self, m, seed):
         out = np.empty(m, dtype=np.float64)

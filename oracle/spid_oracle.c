@@ -117,8 +117,14 @@ int orc_qr(const double* a, size_t m, size_t n, int mode, size_t k, double tol, 
         const double v = orc_norm2(work + j * m, m);
         if (v > max_init) max_init = v;
     }
-    /* BLOCKED rule compares the trailing residual against ||Y||_F */
-    const double yfro = mode == ORC_RULE_BLOCKED ? orc_frobenius(a, m * n) : 0.0;
+    /* BLOCKED rule compares the trailing residual
+     * against ||Y||_F, taken as the column-order sum of per-column
+     * sequential sums of squares. */
+    double yfro = 0.0;
+    if (mode == ORC_RULE_BLOCKED) {
+        for (size_t j = 0; j < n; ++j) yfro += orc_dot(a + j * m, a + j * m, m);
+        yfro = sqrt(yfro);
+    }
     if (max_init < ZERO_FLOOR) {
         st = SPID_ZERO_MATRIX;
         goto done;

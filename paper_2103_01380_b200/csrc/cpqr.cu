@@ -1,0 +1,349 @@
+// cpqr.cu -- batched column ID of small sketches: greedy column-pivoted
+// 2-pass MGS QR + coefficient solve, one subdomain per CTA.
+//
+// Restates, per subdomain, the reference chain
+//   column_id (proj/src/id.cpp:40-45) -> pivoted_mgs_qr / qr_core
+//   (proj/src/qr.cpp:18-124) -> build_coeffs (id.cpp:9-28) ->
+//   solve_upper_triangular (qr.cpp:128-151)
+// with the SAME floating-point operation sequence: every per-column dot
+// product / norm is a sequential left-to-right sum of separately rounded
+// products (one thread per column, __dmul_rn/__dadd_rn, no FMA), so given
+// the same input sketch the pivots, R, C and residual are bit-identical to
+// the reference. Parallelism comes from the columns (one thread each) and
+// from the batch (one CTA per subdomain); the pivot argmax is a warp-shuffle
+// + shared-memory reduction over the total order (norm desc, original index
+// asc) of qr.cpp:68, which any reduction tree resolves identically.
+//
+// Layout: the sketch is transposed into shared memory as W[i][j] (row i
+// contiguous over columns) so that a warp's 32 column-threads read 32
+// consecutive doubles per row -- conflict-free. Columns are never physically
+// swapped: perm[pos] / posof[col] carry the reference's position bookkeeping
+// (qr.cpp:83-87) and R is keyed by original column.
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace spidgpu {
+
+namespace {
+
+constexpr int kCpqrThreads = 256;
+constexpr double kZeroFloor = 1e-300;  // qr.cpp:11
+constexpr double kCollapseRel = 1e-14; // qr.cpp:12
+
+struct CpqrShared {
+    double best_v;
+    int best_i;
+    int stop;
+    int flag;
+    double max_init;
+    double yfro;
+};
+
+template <bool kWInShared>
+__global__ void __launch_bounds__(kCpqrThreads)
+    cpqr_id_kernel(CpqrParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ CpqrShared sh;
+    __shared__ double red_v[kCpqrThreads / kWarp];
+    __shared__ int red_i[kCpqrThreads / kWarp];
+
+    const int b = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int rows = static_cast<int>(p.rows), n = static_cast<int>(p.n);
+    const int npad = p.npad;
+
+    double* W;
+    double* nrm;
+    double* colsq;
+    int* perm;
+    int* posof;
+    {
+        unsigned char* cur = smem_raw;
+        if (kWInShared) {
+            W = reinterpret_cast<double*>(cur);
+            cur += sizeof(double) * static_cast<size_t>(rows) * npad;
+        } else {
+            W = p.w_ws + static_cast<size_t>(b) * rows * npad;
+        }
+        nrm = reinterpret_cast<double*>(cur);
+        cur += sizeof(double) * n;
+        colsq = reinterpret_cast<double*>(cur);
+        cur += sizeof(double) * n;
+        perm = reinterpret_cast<int*>(cur);
+        cur += sizeof(int) * n;
+        posof = reinterpret_cast<int*>(cur);
+    }
+    double* R = p.r_ws + static_cast<size_t>(b) * p.step_cap * n;  // R[s][col]
+    const double* Y = p.Y + static_cast<size_t>(b) * p.strideY;
+
+    // ---- load, transpose, finiteness (qr.cpp:34-35, id.cpp:41-42) -------
+    int bad = 0;
+    const int total = rows * n;
+    for (int e = tid; e < total; e += kCpqrThreads) {
+        const int i = e % rows, j = e / rows;
+        const double v = Y[static_cast<size_t>(j) * p.ldy + i];
+        bad |= !isfinite(v);
+        W[i * npad + j] = v;
+    }
+    for (int j = tid; j < n; j += kCpqrThreads) {
+        perm[j] = j;
+        posof[j] = j;
+    }
+    bad = __syncthreads_or(bad);
+    auto finish_error = [&](int code) {
+        if (tid == 0) {
+            p.status[b] = code;
+            p.rank[b] = 0;
+            p.resid[b] = 0.0;
+        }
+    };
+    if (bad) {
+        finish_error(SPID_NON_FINITE_INPUT);
+        return;
+    }
+    if (p.pre_status != SPID_OK) {  // batch-uniform rule failures (qr.cpp:37-38)
+        finish_error(p.pre_status);
+        return;
+    }
+
+    // ---- initial column norms, max_init (qr.cpp:47-51) -------------------
+    double lmax = 0.0;
+    for (int j = tid; j < n; j += kCpqrThreads) {
+        double s = 0.0;
+        for (int i = 0; i < rows; ++i) {
+            const double w = W[i * npad + j];
+            s = add_rn(s, mul_rn(w, w));
+        }
+        const double v = sqrt(s);
+        nrm[j] = v;
+        colsq[j] = s;
+        lmax = fmax(lmax, v);
+    }
+    lmax = warp_max(lmax);
+    if (lane == 0) red_v[warp] = lmax;
+    __syncthreads();
+    if (tid == 0) {
+        double m = 0.0;
+        for (int w = 0; w < kCpqrThreads / kWarp; ++w) m = fmax(m, red_v[w]);
+        sh.max_init = m;
+        if (p.mode == RULE_BLOCKED) {
+            // ||Y||_F for the blocked rule: per-column sums (in column order)
+            // of sequential per-column squares -- DESIGN.md "cfg4 rule".
+            double f = 0.0;
+            for (int j = 0; j < n; ++j) f = add_rn(f, colsq[j]);
+            sh.yfro = sqrt(f);
+        }
+    }
+    __syncthreads();
+    const double max_init = sh.max_init;
+    if (max_init < kZeroFloor) {
+        finish_error(SPID_ZERO_MATRIX);
+        return;
+    }
+
+    // ---- greedy pivoting loop (qr.cpp:61-106) -----------------------------
+    int rank = 0;
+    const int step_limit = static_cast<int>(p.step_limit);
+    for (int s = 0; s < step_limit; ++s) {
+        // argmax over unselected columns (positions >= s)
+        double bv = -1.0;
+        int bi = 0x7fffffff;
+        for (int j = tid; j < n; j += kCpqrThreads) {
+            if (posof[j] >= s && key_better(nrm[j], j, bv, bi)) {
+                bv = nrm[j];
+                bi = j;
+            }
+        }
+        warp_argmax(bv, bi);
+        if (lane == 0) {
+            red_v[warp] = bv;
+            red_i[warp] = bi;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double v = red_v[0];
+            int ix = red_i[0];
+            for (int w = 1; w < kCpqrThreads / kWarp; ++w)
+                if (key_better(red_v[w], red_i[w], v, ix)) {
+                    v = red_v[w];
+                    ix = red_i[w];
+                }
+            int stop = 0;
+            if (p.mode == RULE_TOL && v <= p.tol * max_init) stop = 1;  // qr.cpp:74-76
+            if (!stop && p.mode == RULE_BLOCKED && s > 0 && s % p.kstep == 0) {
+                double rsq = 0.0;  // residual_fro after s steps, position order (qr.cpp:111-115)
+                for (int pos = s; pos < n; ++pos) {
+                    const double nj = nrm[perm[pos]];
+                    rsq = add_rn(rsq, mul_rn(nj, nj));
+                }
+                if (sqrt(rsq) <= p.tol * sh.yfro) stop = 1;
+            }
+            if (!stop && v < kCollapseRel * max_init)  // qr.cpp:77-81
+                stop = (p.mode == RULE_FIXED && p.strict) ? 2 : 1;
+            if (!stop) {  // position swap (qr.cpp:83-87)
+                const int ps = posof[ix], cs = perm[s];
+                perm[s] = ix;
+                perm[ps] = cs;
+                posof[ix] = s;
+                posof[cs] = ps;
+                R[static_cast<size_t>(s) * n + ix] = v;  // R(s,s) = ||w_s|| (qr.cpp:89-90)
+            }
+            sh.best_v = v;
+            sh.best_i = ix;
+            sh.stop = stop;
+        }
+        __syncthreads();
+        if (sh.stop) {
+            if (sh.stop == 2) {
+                finish_error(SPID_RANK_UNREACHABLE);
+                return;
+            }
+            break;
+        }
+        const int pc = sh.best_i;
+        const double pn = sh.best_v;
+        // q_s = w_s / R(s,s) (qr.cpp:91-92)
+        for (int i = tid; i < rows; i += kCpqrThreads) W[i * npad + pc] = div_rn(W[i * npad + pc], pn);
+        __syncthreads();
+        // two-pass MGS against every unselected column (qr.cpp:94-102); the
+        // next step's fresh norm (qr.cpp:66-67) is accumulated in pass 2.
+        for (int j = tid; j < n; j += kCpqrThreads) {
+            if (posof[j] <= s) continue;
+            double r1 = 0.0;
+            for (int i = 0; i < rows; ++i) r1 = add_rn(r1, mul_rn(W[i * npad + pc], W[i * npad + j]));
+            double r2 = 0.0;
+            for (int i = 0; i < rows; ++i) {
+                const double q = W[i * npad + pc];
+                const double w = sub_rn(W[i * npad + j], mul_rn(r1, q));
+                W[i * npad + j] = w;
+                r2 = add_rn(r2, mul_rn(q, w));
+            }
+            double nn = 0.0;
+            for (int i = 0; i < rows; ++i) {
+                const double w = sub_rn(W[i * npad + j], mul_rn(r2, W[i * npad + pc]));
+                W[i * npad + j] = w;
+                nn = add_rn(nn, mul_rn(w, w));
+            }
+            R[static_cast<size_t>(s) * n + j] = add_rn(r1, r2);
+            nrm[j] = sqrt(nn);
+        }
+        __syncthreads();
+        rank = s + 1;
+    }
+    if (rank == 0) {  // qr.cpp:108-109
+        finish_error(SPID_ZERO_MATRIX);
+        return;
+    }
+
+    // ---- residual_fro (qr.cpp:111-115) and the singular-pivot check -------
+    if (tid == 0) {
+        double rsq = 0.0;
+        for (int pos = rank; pos < n; ++pos) {
+            const double nj = nrm[perm[pos]];
+            rsq = add_rn(rsq, mul_rn(nj, nj));
+        }
+        p.resid[b] = sqrt(rsq);
+        double max_diag = 0.0;  // qr.cpp:135-140
+        for (int t = 0; t < rank; ++t)
+            max_diag = fmax(max_diag, fabs(R[static_cast<size_t>(t) * n + perm[t]]));
+        int sing = 0;
+        for (int t = 0; t < rank; ++t)
+            if (fabs(R[static_cast<size_t>(t) * n + perm[t]]) < 1e-14 * max_diag || max_diag == 0.0)
+                sing = 1;
+        sh.flag = sing;
+    }
+    __syncthreads();
+    if (sh.flag && rank < n) {
+        finish_error(SPID_SINGULAR_PIVOT);
+        return;
+    }
+
+    // ---- coefficients in source column order (id.cpp:9-28) ----------------
+    double* C = p.C + static_cast<size_t>(b) * p.strideC;
+    const int kcap = static_cast<int>(p.kcap);
+    int nonfinite = 0;
+    for (int j = tid; j < n; j += kCpqrThreads) {
+        double* cj = C + static_cast<size_t>(j) * kcap;
+        const int pj = posof[j];
+        if (pj < rank) {  // skeleton column: exact unit vector (id.cpp:12)
+            for (int i = 0; i < rank; ++i) cj[i] = (i == pj) ? 1.0 : 0.0;
+            continue;
+        }
+        // back substitution R11 x = R(:, j) (qr.cpp:143-149), x kept in C
+        for (int ii = rank - 1; ii >= 0; --ii) {
+            double sum = R[static_cast<size_t>(ii) * n + j];
+            for (int jj = ii + 1; jj < rank; ++jj)
+                sum = sub_rn(sum, mul_rn(R[static_cast<size_t>(ii) * n + perm[jj]], cj[jj]));
+            const double x = div_rn(sum, R[static_cast<size_t>(ii) * n + perm[ii]]);
+            cj[ii] = x;
+            nonfinite |= !isfinite(x);
+        }
+    }
+    nonfinite = __syncthreads_or(nonfinite);
+    if (nonfinite) {  // id.cpp:25-26
+        finish_error(SPID_NON_FINITE_COEFFS);
+        return;
+    }
+
+    // ---- outputs ----------------------------------------------------------
+    int64_t* idx = p.indices + static_cast<size_t>(b) * kcap;
+    for (int t = tid; t < rank; t += kCpqrThreads) idx[t] = perm[t];
+    if (p.pivots)
+        for (int pos = tid; pos < n; pos += kCpqrThreads) p.pivots[static_cast<size_t>(b) * n + pos] = perm[pos];
+    if (p.Rout) {  // QrFactorization::r_mat, pivoted order, zero below diagonal
+        double* Ro = p.Rout + static_cast<size_t>(b) * kcap * n;
+        for (int e = tid; e < rank * n; e += kCpqrThreads) {
+            const int i = e % rank, pos = e / rank;
+            Ro[static_cast<size_t>(pos) * kcap + i] =
+                pos < i ? 0.0 : R[static_cast<size_t>(i) * n + perm[pos]];
+        }
+    }
+    if (p.Qout) {
+        double* Qo = p.Qout + static_cast<size_t>(b) * rows * kcap;
+        for (int e = tid; e < rank * rows; e += kCpqrThreads) {
+            const int i = e % rows, t = e / rows;
+            Qo[static_cast<size_t>(t) * rows + i] = W[i * npad + perm[t]];
+        }
+    }
+    if (tid == 0) {
+        p.rank[b] = rank;
+        p.status[b] = SPID_OK;
+    }
+}
+
+}  // namespace
+
+size_t cpqr_smem_bytes(int64_t rows, int64_t n, bool w_in_shared) {
+    size_t bytes = 2 * sizeof(double) * n + 2 * sizeof(int) * n;
+    if (w_in_shared) bytes += sizeof(double) * rows * n;
+    return bytes;
+}
+
+size_t cpqr_max_dyn_smem() { return 200 * 1024; }
+
+cudaError_t launch_cpqr(const CpqrParams& p, bool w_in_shared, cudaStream_t stream) {
+    const size_t smem = cpqr_smem_bytes(p.rows, p.n, w_in_shared);
+    if (w_in_shared) {
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(cpqr_id_kernel<true>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+        }
+        cpqr_id_kernel<true><<<static_cast<unsigned>(p.batch), kCpqrThreads, smem, stream>>>(p);
+    } else {
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(cpqr_id_kernel<false>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+        }
+        cpqr_id_kernel<false><<<static_cast<unsigned>(p.batch), kCpqrThreads, smem, stream>>>(p);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace spidgpu

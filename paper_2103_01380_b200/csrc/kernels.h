@@ -1,0 +1,126 @@
+// kernels.h -- launch interfaces of the spidgpu kernels (host side).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace spidgpu {
+
+enum RuleMode { RULE_FIXED = 0, RULE_TOL = 1, RULE_BLOCKED = 2 };
+
+// ---- CPQR / column ID (cpqr.cu) ------------------------------------------
+struct CpqrParams {
+    const double* Y;
+    int64_t rows, n, ldy, strideY, batch;
+    int mode, strict;
+    int64_t kstep;
+    double tol;
+    int64_t step_limit;  // steps the loop may take (k, min(rows,n), ...)
+    int64_t step_cap;    // rows of the R workspace
+    int64_t kcap;
+    int pre_status;      // batch-uniform failure decided on the host
+    int npad;
+    double* w_ws;        // rows*npad per subdomain when W does not fit smem
+    double* r_ws;        // step_cap*n per subdomain
+    int64_t* indices;
+    double* C;
+    int64_t strideC;
+    int64_t* rank;
+    double* resid;
+    int32_t* status;
+    int64_t* pivots;
+    double* Rout;
+    double* Qout;
+};
+size_t cpqr_smem_bytes(int64_t rows, int64_t n, bool w_in_shared);
+size_t cpqr_max_dyn_smem();
+cudaError_t launch_cpqr(const CpqrParams& p, bool w_in_shared, cudaStream_t stream);
+
+// ---- sketch Y = Omega * A (sketch.cu) -------------------------------------
+struct SketchPlan {
+    int mt;          // M tiles of 8 rows (ell_pad = 8*mt)
+    int nw;          // N tiles of 8 columns per warp
+    int nt;          // columns per CTA tile = 8 warps * 8 * nw
+    int64_t ntiles_col;   // column tiles per subdomain
+    int64_t nchunk;       // 16-row chunks per subdomain
+    int64_t total_chunks; // batch * ntiles_col * nchunk
+    int grid;             // CTAs (persistent, balanced contiguous ranges)
+    int max_segs;         // partial slots per CTA
+    size_t smem;
+    size_t partial_elems; // doubles of the partial workspace
+};
+struct SketchParams {
+    const double* A;
+    int64_t m, n, lda, strideA, batch;
+    int64_t ell;          // rows produced by this launch (<= 8*mt)
+    int64_t row0;         // first Omega row of this launch (ell > 80 is sliced)
+    int omega_mode;       // 0 explicit, 1 philox
+    const double* omega;  // explicit: Omega_s(r, k) at omega + s*stride + k*ldo + r
+    int64_t ldo, stride_o;
+    uint64_t seed;
+    int64_t sub_base;
+    double* partial;      // [grid][max_segs][ell_pad][nt]
+    double* Y;            // final: Y_s(r, j) at Y + s*strideY + j*ldy + (row0 + r)
+    int64_t ldy, strideY;
+};
+bool sketch_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int num_sms,
+                      SketchPlan* plan);
+cudaError_t launch_sketch(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap,
+                          cudaStream_t stream);
+cudaError_t launch_philox_omega(uint64_t seed, int64_t s, int64_t ell, int64_t m, double* out,
+                                int64_t ldo, cudaStream_t stream);
+
+// ---- gathers (gather.cu) --------------------------------------------------
+cudaError_t launch_gather_cols(const double* A, int64_t m, int64_t lda, int64_t strideA,
+                               int64_t batch, const int64_t* indices, int64_t kcap,
+                               const int64_t* rank, int64_t n, double* skel, int64_t ldskel,
+                               int64_t strideS, int32_t* err_flag, cudaStream_t stream);
+cudaError_t launch_gather_rows(const double* A, int64_t m, int64_t n, int64_t lda,
+                               int64_t strideA, int64_t batch, const int64_t* rows,
+                               int64_t nrows, double* B, int64_t ldb, int64_t strideB,
+                               cudaStream_t stream);
+
+// ---- verify / reconstruct (verify.cu) ------------------------------------
+struct VerifyParams {
+    const double* A;
+    int64_t m, n, lda, strideA, batch;
+    const double* skel;
+    int64_t ldskel, strideS;
+    const double* C;
+    int64_t kcap, strideC;
+    const int64_t* rank;
+    double* part;      // [batch][nblk][2] partial sums
+    int64_t nblk;      // row blocks per subdomain
+    double* err2;
+    double* ref2;
+};
+int64_t verify_row_blocks(int64_t m);
+cudaError_t launch_verify(const VerifyParams& p, int num_sms, cudaStream_t stream);
+cudaError_t launch_reconstruct(const double* skel, int64_t m, int64_t ldskel, int64_t strideS,
+                               const double* C, int64_t kcap, int64_t strideC,
+                               const int64_t* rank, int64_t n, int64_t batch, double* out,
+                               int64_t ldo, int64_t strideO, cudaStream_t stream);
+cudaError_t launch_sqdiff(const double* a, const double* b, int64_t count, double* part,
+                          int64_t nparts, cudaStream_t stream);
+
+// ---- synthetic fields (fields.cu) ----------------------------------------
+struct FieldParams {
+    int kind;
+    int64_t grid, block, snapshots;
+    double t_end, nu, sigma;
+    uint64_t seed;
+    int64_t first, batch;
+    double* A;
+    int64_t lda, strideA;
+    // modes: per mode (kx, ky, kz, amp, phase, ax, ay, az) in device memory
+    const double* modes;
+    int n_modes;
+    const double* heavy_modes;
+    int n_heavy;
+    const uint8_t* is_heavy;  // device, batch entries (may be null)
+};
+cudaError_t launch_field(const FieldParams& p, cudaStream_t stream);
+
+}  // namespace spidgpu
