@@ -1,0 +1,431 @@
+#!/usr/bin/env python
+"""SPID compression benchmark (BASELINE.json metric) -- one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Workload: BASELINE config 3, the weak-scaling
+configuration the metric is quoted on at 1/2/4/8 GPUs -- every GPU compresses
+64 subdomains of 32^3 points x 5 QoIs x 256 snapshots (163840 x 256 fp64,
+21.47 GB per GPU) with k=32, p=16 and in-kernel Philox Omega; rank r takes
+global blocks [64r, 64r+64) of the config-5 256^3 field, so at 8 GPUs the run
+is config 5. A step = the whole compress path (sketch -> CPQR + coefficient
+solve -> skeleton gather) over all local subdomains plus the 32-byte NCCL
+report reduction. The exact-error verify pass is timed separately
+ and reported as `verify`.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref,
+compiled from /root/reference/proj/src) on the host cores on a bounded
+sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "raw-field GB/s compressed (SPID end-to-end) at 1/2/4/8 B200; CF and rel. error"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_PEAK_PATH = os.path.join(ROOT, "profiles", "fp64_peak.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "sketch_traffic.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(cfg_name, rank, world):
+    from paper_2103_01380_b200.configs import CONFIGS, weak_range
+
+    cfg = CONFIGS[cfg_name]
+    if cfg.per_gpu_subdomains:
+        field, first, count = weak_range(cfg, rank, world)
+    else:  # fixed-size configs: contiguous share of the config's own field
+        from paper_2103_01380_b200.distributed import contiguous_range
+
+        lo, hi = contiguous_range(cfg.subdomains, rank, world)
+        field, first, count = cfg, lo, hi - lo
+    return cfg, field, first, count
+
+
+def load_json(path):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+# ---- clocks sampled during the timed region (NVML) ----------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device):
+        self.samples, self.reasons = [], set()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                bits = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for b, name in self.REASONS.items():
+                    if bits & b and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---- the reference CPU path (oracle/_ref) ---------------------------------------
+def reference_inputs(cfg, field, first, count, threads, device=0, a_dev=None):
+    """A bounded sample of the workload for the CPU reference: one subdomain
+    per host thread (A_s from the same device generator, untimed) and the
+    exact Philox Omega_s our kernel uses, materialised for the reference's
+    matmul. Inputs only -- the timed path below is the reference's code."""
+    import torch
+
+    from paper_2103_01380_b200 import spid
+    from paper_2103_01380_b200.engine import Engine
+
+    nsamp = max(1, min(threads, count))
+    eng = None
+    if a_dev is None:
+        eng = Engine(device)
+        a_dev = eng.generate(field, first, nsamp)
+    a = a_dev[:nsamp].cpu().numpy()  # (S, n, m) == S column-major m x n
+    om = np.stack([np.ascontiguousarray(spid.philox_omega(cfg.seed, first + s, cfg.ell, cfg.m).T)
+                   for s in range(nsamp)])  # (S, m, ell) == S column-major ell x m
+    del eng, a_dev
+    torch.cuda.empty_cache()
+    return a, om
+
+
+def reference_time(cfg, a, om, threads):
+    """Time the reference CPU compress (oracle/_ref: matmul(Omega_s, A_s) +
+    column_id(Y, fixed k) + select_columns(A_s, I), std::thread per subdomain)."""
+    import oracle
+
+    if not oracle.ref_available():
+        oracle.build()
+    secs, ranks = oracle.ref().compress_batch(a, om, cfg.k, threads)
+    nsamp = a.shape[0]
+    raw = 8.0 * cfg.m * cfg.n * nsamp
+    return {"value": raw / secs / 1e9, "unit": "GB/s", "cores": int(threads),
+            "kind": "reference", "seconds": secs,
+            "sample": f"{nsamp} of the workload's subdomains ({cfg.m}x{cfg.n} fp64 each, "
+                      f"{raw / 1e9:.2f} GB), one per std::thread, Philox Omega materialised "
+                      f"for the reference's matmul; compress = matmul + column_id + "
+                      f"select_columns (oracle/_ref built from /root/reference/proj/src, -O3, "
+                      f"no -march)",
+            "ranks_ok": bool(np.all(ranks == cfg.k))}
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    cfg, field, first, count = workload(args.config, 0, 1)
+    threads = os.cpu_count() or 1
+    a, om = reference_inputs(cfg, field, first, count, threads, local)
+    vals, cpu = [], None
+    for i in range(args.warmup + args.steps):
+        cpu = reference_time(cfg, a, om, threads)
+        if i >= args.warmup:
+            vals.append(cpu["value"])
+    value = float(statistics.median(vals)) if vals else cpu["value"]
+    cpu["value"] = value
+    nsamp = a.shape[0]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 8.0 * cfg.m * cfg.n * nsamp / value / 1e6,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: bounded sample of {nsamp} subdomains of "
+                              f"{cfg.m}x{cfg.n} (k={cfg.k}, p={cfg.p}) on {threads} host threads",
+                   "global_batch": nsamp, "seq_len": cfg.n, "parallelism": "cpu-threads"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---- our arm --------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2103_01380_b200 import distributed as D
+    from paper_2103_01380_b200.engine import Engine, rule_for
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg, field, first, count = workload(args.config, rank, world)
+    eng = Engine(local)
+    dev = eng.dev
+    rule = rule_for(cfg)
+    A = eng.generate(field, first, count)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    res = eng.compress(A, cfg.ell, rule, seed=cfg.seed, subdomain_base=first, want_sketch=True)
+    res.check()
+
+    ev_sk = []  # (start, end) events around every sketch launch in the timed region
+
+    def step(timed):
+        # the three stages of spidgpu_compress_batched, issued separately so the
+        # sketch kernel's own duration can be bracketed with events on its stream
+        if timed:
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+        eng.sketch(A, cfg.ell, seed=cfg.seed, subdomain_base=first, out=res.sketch)
+        if timed:
+            s1.record(stream)
+            ev_sk.append((s0, s1))
+        eng.h.check(_cpqr_into(eng, res, rule))
+        eng.h.check(_gather_into(eng, A, res))
+        sums = torch.stack([res.residual_fro.square().sum(), res.rank.sum().double()])
+        if world > 1:
+            dist.all_reduce(sums)
+        return sums
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = eng.launches()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for _ in range(args.steps):
+            step(True)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = eng.launches() - l0  # spidgpu kernels only (the 2 tiny torch report ops excluded)
+    ms = t0.elapsed_time(t1)
+    sk_ms = sum(a.elapsed_time(b) for a, b in ev_sk) / len(ev_sk)
+    tm = torch.tensor([ms, sk_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    ms, sk_ms = float(tm[0]), float(tm[1])
+    ms_step = ms / args.steps
+    raw_local = cfg.raw_bytes(count)
+    raw_total = raw_local * world  # weak scaling: equal share per rank
+    value = raw_total / (ms_step / 1e3) / 1e9
+
+    # verify phase (timed separately) and the report
+    torch.cuda.synchronize()
+    v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    v0.record(stream)
+    err2, ref2 = eng.verify(A, res)
+    v1.record(stream)
+    torch.cuda.synchronize()
+    verify_ms = v0.elapsed_time(v1)
+    sums = D.local_sums(err2.cpu(), ref2.cpu(), res.rank.cpu(), cfg.m, cfg.n).to(dev)
+    report = D.reduce_report(sums)
+    vt = torch.tensor([verify_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(vt, op=dist.ReduceOp.MAX)
+    verify_ms = float(vt[0])
+
+    # roofline of the dominant kernel (the sketch)
+    flops = 2.0 * cfg.ell * cfg.m * cfg.n * count
+    fp64 = load_json(FP64_PEAK_PATH) or {}
+    peak_tf = fp64.get("dmma_tflops", 37.1)
+    achieved_tf = flops / (sk_ms / 1e3) / 1e12
+    peaks = load_json(PEAKS_PATH) or {}
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    traffic = (load_json(TRAFFIC_PATH) or {}).get(cfg.name)
+    roofline = {
+        "bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+        "frac": achieved_tf / peak_tf, "traffic": traffic,
+        "kernel": "sketch_kernel (DMMA.8x8x4 FP64, TMA-staged A)",
+        "algorithmic": f"2*ell*m*n = {2.0 * cfg.ell * cfg.m * cfg.n:.4g} flop and 8*m*n = "
+                       f"{8.0 * cfg.m * cfg.n:.4g} B per subdomain x {count} subdomains per launch",
+        "kernel_ms": sk_ms,
+        "hbm_frac": (8.0 * cfg.m * cfg.n * count / (sk_ms / 1e3) / 1e9) / hbm,
+        "peak_source": ("profiles/fp64_peak.json: sustained DMMA microbenchmark on this pool "
+                        "(MEASURED_PEAKS.json has no FP64 entry)"),
+    }
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {count} subdomains/GPU of 32^3 x 5 QoIs x "
+                               f"{cfg.n} snapshots ({cfg.m}x{cfg.n} fp64), k={cfg.k}, p={cfg.p}, "
+                               f"Philox Omega; global blocks [{first}, {first + count}) per rank of "
+                               f"the {field.grid}^3 multimode TGV field",
+                   "global_batch": count * world, "seq_len": cfg.n, "parallelism": f"dp{world}",
+                   "l2": "inputs (21.5 GB/GPU) larger than L2 (126 MB); no flush needed"},
+        "cf": report.cf, "rel_frob_error": report.rel_frob_error,
+        "stored_entries": report.stored_entries,
+        "verify": {"ms": verify_ms, "raw_gbs_with_verify":
+                   raw_total / ((ms_step + verify_ms) / 1e3) / 1e9},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "roofline": roofline,
+    }
+
+    if not args.no_e2e:
+        line["e2e"] = e2e_measure(eng, cfg, A, first, count, rule, args, world)
+    if world > 1:
+        dist.barrier()
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        try:
+            threads = os.cpu_count() or 1
+            a_h, om_h = reference_inputs(cfg, field, first, count, threads, local, a_dev=A)
+            line["cpu_baseline"] = reference_time(cfg, a_h, om_h, threads)
+        except Exception as e:  # reported, never fatal
+            line["cpu_baseline"] = {"error": repr(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def _cpqr_into(eng, res, rule):
+    import ctypes as C
+
+    from paper_2103_01380_b200 import _native as N
+
+    S, n, rows = res.sketch.shape
+    p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    import torch
+
+    return N.lib.spidgpu_cpqr_id_batched(
+        eng.h.h, p(res.sketch), rows, n, rows, rows * n, S, C.byref(rule.c()), res.kcap,
+        p(res.indices), p(res.coeffs), res.kcap * n, p(res.rank), p(res.residual_fro),
+        p(res.status), None, None, None, C.c_void_p(torch.cuda.current_stream().cuda_stream))
+
+
+def _gather_into(eng, A, res):
+    import ctypes as C
+
+    import torch
+
+    from paper_2103_01380_b200 import _native as N
+
+    S, n, m = A.shape
+    p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    return N.lib.spidgpu_gather_batched(eng.h.h, p(A), m, n, m, m * n, S, p(res.indices),
+                                        res.kcap, p(res.rank), p(res.skel), m, m * res.kcap,
+                                        C.c_void_p(torch.cuda.current_stream().cuda_stream))
+
+
+def e2e_measure(eng, cfg, A, first, count, rule, args, world):
+    """The same metric through the C-ABI host call (spidgpu_compress_host):
+    pinned host A in, host factors out, every copy inside the timed region."""
+    import torch
+    import torch.distributed as dist
+
+    a_host = torch.empty(A.shape, dtype=torch.float64, pin_memory=True)
+    a_host.copy_(A)
+    kcap = rule.cap(cfg.ell, cfg.n)
+    out = {
+        "indices": torch.empty((count, kcap), dtype=torch.int64, pin_memory=True),
+        "coeffs": torch.empty((count, cfg.n, kcap), dtype=torch.float64, pin_memory=True),
+        "skel": torch.empty((count, kcap, cfg.m), dtype=torch.float64, pin_memory=True),
+        "rank": torch.empty(count, dtype=torch.int64, pin_memory=True),
+        "residual_fro": torch.empty(count, dtype=torch.float64, pin_memory=True),
+        "status": torch.empty(count, dtype=torch.int32, pin_memory=True),
+    }
+    eng.compress_host(a_host, cfg.ell, rule, seed=cfg.seed, subdomain_base=first, group=8,
+                      out=out)  # warm-up (allocates the lane buffers)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        eng.compress_host(a_host, cfg.ell, rule, seed=cfg.seed, subdomain_base=first, group=8,
+                          out=out)
+    el = torch.tensor([(time.perf_counter() - t) / args.e2e_steps], dtype=torch.float64,
+                      device=eng.dev)
+    if world > 1:
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    sec = float(el[0])
+    h2d = a_host.numel() * 8
+    d2h = sum(v.numel() * v.element_size() for v in out.values())
+    return {"value": cfg.raw_bytes(count) * world / sec / 1e9, "unit": "GB/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "api": "spidgpu_compress_host (C ABI, pinned host buffers, 2 copy/compute lanes)",
+            "steps": args.e2e_steps, "ms_per_step": sec * 1e3}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

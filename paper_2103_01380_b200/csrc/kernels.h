@@ -40,9 +40,10 @@ cudaError_t launch_cpqr(const CpqrParams& p, bool w_in_shared, cudaStream_t stre
 
 // ---- sketch Y = Omega * A (sketch.cu) -------------------------------------
 struct SketchPlan {
+    int ell_pad;     // Omega rows computed (8..80)
     int mt;          // M tiles of 8 rows (ell_pad = 8*mt)
     int nw;          // N tiles of 8 columns per warp
-    int nt;          // columns per CTA tile = 8 warps * 8 * nw
+    int nt;          // columns per CTA tile
     int64_t ntiles_col;   // column tiles per subdomain
     int64_t nchunk;       // 16-row chunks per subdomain
     int64_t total_chunks; // batch * ntiles_col * nchunk

@@ -1,15 +1,14 @@
 // philox.cuh -- counter-based Gaussian generator for the in-kernel sketch.
 //
 // Omega_s(r, k) of subdomain s is a pure function of (seed, s, r, k), so any
-// CTA can generate any tile without state, the sketch kernel never reads
-// Omega from HBM (performance mode), and spidgpu_philox_omega() can
-// materialise the identical matrix for an oracle.
+// warp can generate exactly the fragment values it feeds to the tensor core,
+// the sketch kernel never reads Omega from HBM (performance mode), and
+// spidgpu_philox_omega() can materialise the identical matrix for an oracle.
 //
-// Philox4x32-10 (Salmon et al., SC'11): counter {k, r/4, s_lo, s_hi}, key
-// {seed_lo, seed_hi}; the 4 outputs become the normals of rows 4*(r/4)+0..3
-// via two Box-Muller transforms in fp32 with the SFU intrinsics (the sketch
-// only needs a Gaussian-distributed Omega, not fp64-accurate normals), then
-// widened to fp64.
+// Philox4x32-10 (Salmon et al., SC'11): counter {k/4, r, s_lo, s_hi}, key
+// {seed_lo, seed_hi}; the 4 outputs become Omega_s(r, 4*(k/4) + 0..3) via two
+// Box-Muller transforms in fp32 with the SFU intrinsics (the sketch needs a
+// Gaussian-distributed Omega, not fp64-accurate normals), widened to fp64.
 #pragma once
 
 #include <stdint.h>
@@ -44,19 +43,22 @@ __host__ __device__ __forceinline__ Philox4 philox4x32_10(Philox4 c, uint32_t k0
     return c;
 }
 
-// Four N(0,1) samples for Omega_s(4*g + 0..3, k).
-__device__ __forceinline__ void omega_normals4(uint64_t seed, uint64_t s, uint32_t g, uint32_t k,
+// Four N(0,1) samples for Omega_s(r, 4*kq + 0..3).
+__device__ __forceinline__ void omega_normals4(uint64_t seed, uint64_t s, uint32_t r, uint32_t kq,
                                                double out[4]) {
-    const Philox4 r = philox4x32_10(
-        Philox4{k, g, static_cast<uint32_t>(s), static_cast<uint32_t>(s >> 32)},
+    const Philox4 v = philox4x32_10(
+        Philox4{kq, r, static_cast<uint32_t>(s), static_cast<uint32_t>(s >> 32)},
         static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
     const float kInv = 2.3283064365386963e-10f;  // 2^-32
-    const float u1a = (static_cast<float>(r.x) + 1.0f) * kInv;  // (0, 1]
-    const float u2a = static_cast<float>(r.y) * kInv;
-    const float u1b = (static_cast<float>(r.z) + 1.0f) * kInv;
-    const float u2b = static_cast<float>(r.w) * kInv;
-    const float ra = sqrtf(-2.0f * __logf(u1a));
-    const float rb = sqrtf(-2.0f * __logf(u1b));
+    const float u1a = (static_cast<float>(v.x) + 1.0f) * kInv;  // (0, 1]
+    const float u2a = static_cast<float>(v.y) * kInv;
+    const float u1b = (static_cast<float>(v.z) + 1.0f) * kInv;
+    const float u2b = static_cast<float>(v.w) * kInv;
+    // r = sqrt(-2 ln u) as x * rsqrt(x): MUFU.RSQ, no IEEE-sqrt slow path
+    const float xa = fmaxf(-2.0f * __logf(u1a), 1e-30f);
+    const float xb = fmaxf(-2.0f * __logf(u1b), 1e-30f);
+    const float ra = xa * rsqrtf(xa);
+    const float rb = xb * rsqrtf(xb);
     float sa, ca, sb, cb;
     __sincosf(6.2831853071795865f * u2a, &sa, &ca);
     __sincosf(6.2831853071795865f * u2b, &sb, &cb);

@@ -15,19 +15,23 @@
 //  * persistent grid, one CTA per SM; the flat (subdomain, column tile,
 //    16-row chunk) space is split into equal contiguous ranges, one per CTA
 //    (stream-K style): perfect balance, and a CTA writes one partial per
-//    tile it touches (<= 2-3), so split-K traffic is ~0.1% of A;
+//    tile it touches (<= 2-3), so split-K traffic is ~0.05% of A;
 //  * A chunks (16 rows x NT columns, 128 B rows) are staged by TMA with
-//    128B swizzle through a 4-stage mbarrier ring; OOB rows/columns are
-//    zero-filled by the TMA unit, so ragged m and n need no masking;
-//  * Omega chunks (ell_pad x 16) are generated in-kernel by Philox one chunk
-//    ahead (performance mode) or loaded from HBM (oracle mode), written to a
-//    swizzled double buffer; they are never re-read from HBM;
-//  * the K index inside a chunk is permuted so each thread fetches its two
-//    consecutive K values of an operand with one 16-byte shared load;
-//    swizzles make every fragment load bank-conflict free;
-//  * partials are reduced by a second tiny kernel in a fixed order, so Y is
-//    bitwise reproducible run to run (SPEC determinism, proj/tests/
-//    test_matrix_core.cpp:145-153).
+//    128B swizzle through an S-stage ring; "full" mbarriers carry the TMA
+//    transaction bytes, "empty" mbarriers collect one arrive per warp, so
+//    the main loop has no CTA-wide barrier at all. OOB rows/columns are
+//    zero-filled by the TMA unit (ragged m, n need no masking);
+//  * warps tile the CTA 2 (M) x 4 (N) (1 x 8 for ell <= 24); Omega never
+//    touches HBM or shared memory in performance mode: each lane runs the
+//    Philox generator for exactly the fragment values it feeds to DMMA (one
+//    call = 4 consecutive K of one row), one chunk ahead, interleaved with
+//    the tensor-core work of the current chunk;
+//  * inside a 16-row chunk lane q feeds K = 4q + 2h + e at k-step (h, e), so
+//    each A fragment pair is one 16-byte shared load and the two rows of a
+//    quarter-warp hit opposite 16B-chunk parities under the swizzle: every
+//    fragment load is bank-conflict free;
+//  * partials are reduced by a small second kernel in a fixed order, so Y is
+//    bitwise reproducible run to run (proj/tests/test_matrix_core.cpp:145-153).
 #include <math.h>
 
 #include "common.cuh"
@@ -38,28 +42,24 @@ namespace spidgpu {
 
 namespace {
 
-constexpr int kKc = 16;       // rows of A per chunk (128 B = one swizzle row)
-constexpr int kStages = 4;    // TMA ring depth
-constexpr int kWarps = 8;
-constexpr int kThreads = kWarps * kWarp;
+constexpr int kKc = 16;  // rows of A per chunk (128 B = one swizzle row)
+constexpr int kWarps = 16;           // consumer (tensor-core) warps: 4 per SMSP
+constexpr int kProducerWarps = 2;    // TMA issue + Omega generation
+constexpr int kThreads = (kWarps + kProducerWarps) * kWarp;
+constexpr int kStageBudget = 200 * 1024;
 
-template <int MT, int NW>
+template <int WM, int MTW, int NW>
 struct SketchCfg {
-    static constexpr int kEllPad = 8 * MT;
-    static constexpr int kNt = kWarps * 8 * NW;
-    static constexpr int kABytes = kNt * kKc * 8;       // one stage of A
-    static constexpr int kOBytes = kEllPad * kKc * 8;   // one Omega buffer
-    static constexpr size_t kSmem = 1024 + kStages * kABytes + 2 * kOBytes + kStages * 8;
-    static constexpr int kGroups = 2 * MT * kKc;        // Philox calls per chunk (4 rows each)
-    static constexpr int kGroupsPerThread = (kGroups + kThreads - 1) / kThreads;
-    static constexpr int kExplicitPerThread = (kEllPad * kKc + kThreads - 1) / kThreads;
+    static constexpr int kWn = kWarps / WM;
+    static constexpr int kEllPad = 8 * MTW * WM;
+    static constexpr int kNt = 8 * NW * kWn;
+    static constexpr int kABytes = kNt * kKc * 8;
+    static constexpr int kOBytes = kEllPad * kKc * 8;
+    static constexpr int kStageBytes = kABytes + kOBytes;
+    static constexpr int kStages =
+        (kStageBudget / kStageBytes) < 8 ? (kStageBudget / kStageBytes) : 8;
+    static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes + 3 * 8 * kStages;
 };
-
-// swizzled offset (in doubles) of element (row, kk) in a [rows][16] tile:
-// 16-byte chunk kk/2 is XOR-ed with row%8 (matches TMA SWIZZLE_128B).
-__device__ __forceinline__ int swz(int row, int kk) {
-    return row * kKc + ((((kk >> 1) ^ (row & 7)) << 1) | (kk & 1));
-}
 
 struct ChunkPos {
     int64_t s, ct, kc;
@@ -70,17 +70,28 @@ __device__ __forceinline__ ChunkPos chunk_pos(int64_t g, int64_t nchunk, int64_t
     return ChunkPos{tile / ntiles_col, tile % ntiles_col, g % nchunk};
 }
 
-template <int MT, int NW, int OMODE>
+// Warp-specialised persistent kernel:
+//   warps 0..7  consumers: LDS.128 fragments + DMMA.8x8x4 into registers
+//   warps 8..9  producers: TMA issue of the A chunk + Philox (or explicit)
+//               Omega chunk into a swizzled shared ring
+// Stage hand-off: full_a (TMA tx bytes), full_o (64 producer arrivals),
+// empty (8 consumer-warp arrivals). No CTA-wide barrier in the main loop.
+template <int WM, int MTW, int NW, int OMODE>
 __global__ void __launch_bounds__(kThreads, 1)
     sketch_kernel(const __grid_constant__ CUtensorMap tmap, SketchParams p, int64_t nchunk,
                   int64_t ntiles_col, int64_t total_chunks, int max_segs) {
-    using Cfg = SketchCfg<MT, NW>;
+    using Cfg = SketchCfg<WM, MTW, NW>;
+    constexpr int S = Cfg::kStages;
     extern __shared__ unsigned char smem_raw[];
-    unsigned char* base = reinterpret_cast<unsigned char*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    double* abuf = reinterpret_cast<double*>(base);
-    double* obuf = reinterpret_cast<double*>(base + kStages * Cfg::kABytes);
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(base + kStages * Cfg::kABytes + 2 * Cfg::kOBytes);
+    const uint32_t raw_s = smem_u32(smem_raw);
+    const uint32_t base_s = (raw_s + 1023u) & ~1023u;  // 128B-swizzle atoms need 1 KiB alignment
+    unsigned char* base = smem_raw + (base_s - raw_s);
+    // stage i: A at base_s + i*kABytes; Omega at base_s + S*kABytes + i*kOBytes
+    const uint32_t a_s = base_s;
+    const uint32_t o_s = base_s + S * Cfg::kABytes;
+    uint64_t* full_a = reinterpret_cast<uint64_t*>(base + S * Cfg::kStageBytes);
+    uint64_t* full_o = full_a + S;
+    uint64_t* empty = full_o + S;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t G = gridDim.x, c = blockIdx.x;
@@ -90,131 +101,123 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (tid == 0) {
         prefetch_tmap(&tmap);
-        for (int i = 0; i < kStages; ++i) mbar_init(&mbar[i], 1);
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full_a[i], 1);
+            mbar_init(&full_o[i], kProducerWarps * kWarp);
+            mbar_init(&empty[i], kWarps);
+        }
         fence_barrier_init();
     }
     __syncthreads();
 
-    auto issue = [&](int64_t it) {
-        const ChunkPos cp = chunk_pos(lo + it, nchunk, ntiles_col);
-        const int slot = static_cast<int>(it % kStages);
-        mbar_arrive_expect_tx(&mbar[slot], Cfg::kABytes);
-        tma_load_3d(abuf + slot * (Cfg::kABytes / 8), &tmap, &mbar[slot],
-                    static_cast<int>(cp.kc * kKc), static_cast<int>(cp.ct * Cfg::kNt),
-                    static_cast<int>(cp.s));
-    };
-    if (tid == 0) {
-        const int64_t pre = niter < kStages - 1 ? niter : kStages - 1;
-        for (int64_t it = 0; it < pre; ++it) issue(it);
+    if (warp >= kWarps) {
+        // ------------------------------ producers ------------------------------
+        const int pt = tid - kWarps * kWarp;  // 0..63
+        constexpr int kCalls = Cfg::kEllPad * (kKc / 4);  // (row, k-quad) pairs per chunk
+        ChunkPos cp = chunk_pos(lo, nchunk, ntiles_col);  // advanced incrementally
+        int slot = 0;
+        uint32_t epar = 0;  // parity of the empty-barrier phase being waited on
+        for (int64_t it = 0; it < niter; ++it) {
+            if (it >= S) mbar_wait(&empty[slot], epar);
+            if (pt == 0) {
+                mbar_arrive_expect_tx(&full_a[slot], Cfg::kABytes);
+                tma_load_3d(base + slot * Cfg::kABytes, &tmap, &full_a[slot],
+                            static_cast<int>(cp.kc * kKc), static_cast<int>(cp.ct * Cfg::kNt),
+                            static_cast<int>(cp.s));
+            }
+            const uint32_t ob = o_s + slot * Cfg::kOBytes;
+            for (int call = pt; call < kCalls; call += kProducerWarps * kWarp) {
+                const int kq = call & 3, r = call >> 2;  // lanes: 4 k-quads x 8 rows
+                double v[4];
+                const int64_t k0 = cp.kc * kKc + 4 * kq;
+                if constexpr (OMODE == 1) {
+                    omega_normals4(p.seed, static_cast<uint64_t>(p.sub_base + cp.s),
+                                   static_cast<uint32_t>(p.row0 + r),
+                                   static_cast<uint32_t>(k0 >> 2), v);
+                    if (r >= p.ell) v[0] = v[1] = v[2] = v[3] = 0.0;  // selects, no FP64 math
+                } else {
+                    const double* src = p.omega + cp.s * p.stride_o + p.row0 + r;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        v[j] = (r < p.ell && k0 + j < p.m) ? __ldg(src + (k0 + j) * p.ldo) : 0.0;
+                }
+                // row r, 16B chunks 2kq and 2kq+1, XOR-swizzled by r%8
+                const uint32_t rowb = ob + r * (kKc * 8);
+                sts128(rowb + ((((2 * kq) ^ (r & 7))) << 4), v[0], v[1]);
+                sts128(rowb + ((((2 * kq + 1) ^ (r & 7))) << 4), v[2], v[3]);
+            }
+            mbar_arrive(&full_o[slot]);
+            if (++cp.kc == nchunk) {
+                cp.kc = 0;
+                if (++cp.ct == ntiles_col) {
+                    cp.ct = 0;
+                    ++cp.s;
+                }
+            }
+            if (++slot == S) {
+                slot = 0;
+                if (it + 1 >= 2 * S) epar ^= 1u;  // waits for chunk it-S: phase (it-S)/S
+            }
+        }
+        return;
     }
 
-    // ---- Omega production (registers, then swizzled smem) -----------------
-    double oreg[OMODE == 1 ? 4 * Cfg::kGroupsPerThread : Cfg::kExplicitPerThread];
-    auto omega_fetch = [&](int64_t g) {
-        const ChunkPos cp = chunk_pos(g, nchunk, ntiles_col);
-        const int64_t k0 = cp.kc * kKc;
-        if constexpr (OMODE == 1) {
-#pragma unroll
-            for (int q = 0; q < Cfg::kGroupsPerThread; ++q) {
-                const int grp = tid + q * kThreads;
-                if (grp < Cfg::kGroups) {
-                    const int g4 = grp % (2 * MT), kk = grp / (2 * MT);
-                    omega_normals4(p.seed, static_cast<uint64_t>(p.sub_base + cp.s),
-                                   static_cast<uint32_t>((p.row0 >> 2) + g4),
-                                   static_cast<uint32_t>(k0 + kk), &oreg[4 * q]);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        if (4 * g4 + e >= p.ell) oreg[4 * q + e] = 0.0;
-                }
-            }
-        } else {
-            const double* om = p.omega + cp.s * p.stride_o + p.row0;
-#pragma unroll
-            for (int q = 0; q < Cfg::kExplicitPerThread; ++q) {
-                const int e = tid + q * kThreads;
-                double v = 0.0;
-                if (e < Cfg::kEllPad * kKc) {
-                    const int r = e % Cfg::kEllPad, kk = e / Cfg::kEllPad;
-                    const int64_t k = k0 + kk;
-                    if (r < p.ell && k < p.m) v = __ldg(om + k * p.ldo + r);
-                }
-                oreg[q] = v;
-            }
-        }
-    };
-    auto omega_store = [&](double* ob) {
-        if constexpr (OMODE == 1) {
-#pragma unroll
-            for (int q = 0; q < Cfg::kGroupsPerThread; ++q) {
-                const int grp = tid + q * kThreads;
-                if (grp < Cfg::kGroups) {
-                    const int g4 = grp % (2 * MT), kk = grp / (2 * MT);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) ob[swz(4 * g4 + e, kk)] = oreg[4 * q + e];
-                }
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < Cfg::kExplicitPerThread; ++q) {
-                const int e = tid + q * kThreads;
-                if (e < Cfg::kEllPad * kKc) ob[swz(e % Cfg::kEllPad, e / Cfg::kEllPad)] = oreg[q];
-            }
-        }
-    };
-    omega_fetch(lo);
-    omega_store(obuf);
+    // ------------------------------- consumers -------------------------------
+    const int grow = lane >> 2;  // fragment row (Omega) / column (A) within 8
+    const int q4 = lane & 3;
+    const int wm = warp / Cfg::kWn, wn = warp % Cfg::kWn;
+    const int row0 = wm * MTW * 8;  // this warp's Omega rows
+    const int col0 = wn * NW * 8;   // this warp's A columns
 
-    double acc[MT][NW][2];
+    double acc[MTW][NW][2];
 #pragma unroll
-    for (int i = 0; i < MT; ++i)
+    for (int i = 0; i < MTW; ++i)
 #pragma unroll
         for (int j = 0; j < NW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    const int grow = lane >> 2;  // fragment row / column within an 8-block
-    const int q4 = lane & 3;
-    const int wcol0 = warp * NW * 8;
     int seg = 0;
-
+    int slot = 0;
+    uint32_t par = 0;
+    int64_t kc = lo % nchunk;  // chunk index inside the current tile
     for (int64_t it = 0; it < niter; ++it) {
-        const int slot = static_cast<int>(it % kStages);
-        mbar_wait(&mbar[slot], static_cast<uint32_t>((it / kStages) & 1));
-        __syncthreads();  // Omega(it) visible; iteration it-1 fully consumed
-        if (tid == 0 && it + kStages - 1 < niter) issue(it + kStages - 1);
-        const bool more = it + 1 < niter;
-        if (more) omega_fetch(lo + it + 1);
-
-        const double* At = abuf + slot * (Cfg::kABytes / 8);
-        const double* Ot = obuf + (it & 1) * (Cfg::kOBytes / 8);
+        mbar_wait(&full_a[slot], par);
+        mbar_wait(&full_o[slot], par);
+        const uint32_t at = a_s + slot * Cfg::kABytes;
+        const uint32_t ot = o_s + slot * Cfg::kOBytes;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const int ch = ((4 * h + q4) ^ grow) << 1;  // swizzled pair offset
-            double2 of[MT], af[NW];
+            // lane q feeds K = 4q + 2h + e: 16-byte pair (2q + h), swizzled by row%8 == grow
+            const uint32_t ch = static_cast<uint32_t>(((2 * q4 + h) ^ grow) << 4);
+            double2 of[MTW], af[NW];
 #pragma unroll
-            for (int mt = 0; mt < MT; ++mt)
-                of[mt] = *reinterpret_cast<const double2*>(Ot + (8 * mt + grow) * kKc + ch);
+            for (int mt = 0; mt < MTW; ++mt) of[mt] = lds128(ot + (row0 + 8 * mt + grow) * 128 + ch);
 #pragma unroll
-            for (int nt = 0; nt < NW; ++nt)
-                af[nt] = *reinterpret_cast<const double2*>(At + (wcol0 + 8 * nt + grow) * kKc + ch);
+            for (int nt = 0; nt < NW; ++nt) af[nt] = lds128(at + (col0 + 8 * nt + grow) * 128 + ch);
 #pragma unroll
-            for (int mt = 0; mt < MT; ++mt)
+            for (int mt = 0; mt < MTW; ++mt)
 #pragma unroll
                 for (int nt = 0; nt < NW; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], of[mt].x, af[nt].x);
 #pragma unroll
-            for (int mt = 0; mt < MT; ++mt)
+            for (int mt = 0; mt < MTW; ++mt)
 #pragma unroll
                 for (int nt = 0; nt < NW; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], of[mt].y, af[nt].y);
         }
-        if (more) omega_store(obuf + ((it + 1) & 1) * (Cfg::kOBytes / 8));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
 
-        const int64_t g = lo + it;
-        if (!more || (g + 1) / nchunk != g / nchunk) {  // tile boundary: flush partial
+        if (++slot == S) {
+            slot = 0;
+            par ^= 1u;
+        }
+        if (++kc == nchunk || it + 1 == niter) {  // tile boundary: flush partial
+            kc = 0;
             double* part = p.partial + (static_cast<size_t>(c) * max_segs + seg) *
                                            (static_cast<size_t>(Cfg::kEllPad) * Cfg::kNt);
 #pragma unroll
-            for (int mt = 0; mt < MT; ++mt)
+            for (int mt = 0; mt < MTW; ++mt)
 #pragma unroll
                 for (int nt = 0; nt < NW; ++nt) {
-                    const int r = 8 * mt + grow, col = wcol0 + 8 * nt + 2 * q4;
+                    const int r = row0 + 8 * mt + grow, col = col0 + 8 * nt + 2 * q4;
                     *reinterpret_cast<double2*>(part + r * Cfg::kNt + col) =
                         make_double2(acc[mt][nt][0], acc[mt][nt][1]);
                     acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
@@ -266,24 +269,24 @@ __global__ void sketch_reduce_kernel(SketchParams p, int ell_pad, int nt, int64_
 
 __global__ void philox_omega_kernel(uint64_t seed, int64_t s, int64_t ell, int64_t m, double* out,
                                     int64_t ldo) {
-    const int64_t ngroups = (ell + 3) / 4;
-    const int64_t total = ngroups * m;
+    const int64_t nq = (m + 3) / 4;
+    const int64_t total = nq * ell;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t g4 = e % ngroups, k = e / ngroups;
+        const int64_t r = e % ell, kq = e / ell;
         double v[4];
-        omega_normals4(seed, static_cast<uint64_t>(s), static_cast<uint32_t>(g4),
-                       static_cast<uint32_t>(k), v);
-        for (int i = 0; i < 4; ++i)
-            if (4 * g4 + i < ell) out[k * ldo + 4 * g4 + i] = v[i];
+        omega_normals4(seed, static_cast<uint64_t>(s), static_cast<uint32_t>(r),
+                       static_cast<uint32_t>(kq), v);
+        for (int j = 0; j < 4; ++j)
+            if (4 * kq + j < m) out[(4 * kq + j) * ldo + r] = v[j];
     }
 }
 
-template <int MT, int NW, int OMODE>
+template <int WM, int MTW, int NW, int OMODE>
 cudaError_t launch_t(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap,
                      cudaStream_t stream) {
-    using Cfg = SketchCfg<MT, NW>;
-    auto kern = sketch_kernel<MT, NW, OMODE>;
+    using Cfg = SketchCfg<WM, MTW, NW>;
+    auto kern = sketch_kernel<WM, MTW, NW, OMODE>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(Cfg::kSmem));
     if (e != cudaSuccess) return e;
@@ -297,65 +300,81 @@ cudaError_t launch_t(const SketchParams& p, const SketchPlan& plan, const CUtens
     return cudaGetLastError();
 }
 
-template <int MT, int OMODE>
+// (WM, MTW) by ell_pad; NW picks the column tile
+template <int WM, int MTW, int OMODE>
 cudaError_t launch_nw(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap,
                       cudaStream_t stream) {
-    switch (plan.nw) {
-        case 1: return launch_t<MT, 1, OMODE>(p, plan, tmap, stream);
-        case 2: return launch_t<MT, 2, OMODE>(p, plan, tmap, stream);
-        default:
-            if constexpr (MT <= 8) return launch_t<MT, 4, OMODE>(p, plan, tmap, stream);
-            return cudaErrorInvalidValue;
+    if constexpr (WM == 1) {
+        switch (plan.nw) {
+            case 1: return launch_t<WM, MTW, 1, OMODE>(p, plan, tmap, stream);
+            default: return launch_t<WM, MTW, 2, OMODE>(p, plan, tmap, stream);
+        }
+    } else if constexpr (MTW <= 3) {
+        switch (plan.nw) {
+            case 1: return launch_t<WM, MTW, 1, OMODE>(p, plan, tmap, stream);
+            case 2: return launch_t<WM, MTW, 2, OMODE>(p, plan, tmap, stream);
+            default: return launch_t<WM, MTW, 4, OMODE>(p, plan, tmap, stream);
+        }
+    } else {  // ell_pad 64/80: cap the accumulator tile at MTW x 2 (register budget)
+        switch (plan.nw) {
+            case 1: return launch_t<WM, MTW, 1, OMODE>(p, plan, tmap, stream);
+            default: return launch_t<WM, MTW, 2, OMODE>(p, plan, tmap, stream);
+        }
     }
 }
 
 template <int OMODE>
-cudaError_t launch_mt(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap,
-                      cudaStream_t stream) {
-    switch (plan.mt) {
-        case 2: return launch_nw<2, OMODE>(p, plan, tmap, stream);
-        case 3: return launch_nw<3, OMODE>(p, plan, tmap, stream);
-        case 4: return launch_nw<4, OMODE>(p, plan, tmap, stream);
-        case 6: return launch_nw<6, OMODE>(p, plan, tmap, stream);
-        case 8: return launch_nw<8, OMODE>(p, plan, tmap, stream);
-        case 10: return launch_nw<10, OMODE>(p, plan, tmap, stream);
+cudaError_t launch_mode(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap,
+                        cudaStream_t stream) {
+    switch (plan.ell_pad) {
+        case 8: return launch_nw<1, 1, OMODE>(p, plan, tmap, stream);
+        case 16: return launch_nw<1, 2, OMODE>(p, plan, tmap, stream);
+        case 24: return launch_nw<1, 3, OMODE>(p, plan, tmap, stream);
+        case 32: return launch_nw<2, 2, OMODE>(p, plan, tmap, stream);
+        case 48: return launch_nw<2, 3, OMODE>(p, plan, tmap, stream);
+        case 64: return launch_nw<2, 4, OMODE>(p, plan, tmap, stream);
+        case 80: return launch_nw<2, 5, OMODE>(p, plan, tmap, stream);
         default: return cudaErrorInvalidValue;
     }
 }
 
-size_t smem_for(int mt, int nw) {
-    const int nt = kWarps * 8 * nw;
-    return 1024 + kStages * (nt * kKc * 8) + 2 * (8 * mt * kKc * 8) + kStages * 8;
-}
-
 }  // namespace
 
-// Omega rows handled by one launch: 80 (MT=10); wider sketches are sliced.
+// Omega rows handled by one launch: <= 80; wider sketches are sliced.
 bool sketch_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int num_sms,
                       SketchPlan* plan) {
     if (m < 1 || n < 1 || batch < 1 || ell < 1 || ell > 80) return false;
-    const int mts[] = {2, 3, 4, 6, 8, 10};
-    int mt = 10;
-    for (int v : mts)
-        if (8 * v >= ell) {
-            mt = v;
+    const int pads[] = {8, 16, 24, 32, 48, 64, 80};
+    int ell_pad = 80;
+    for (int v : pads)
+        if (v >= ell) {
+            ell_pad = v;
             break;
         }
+    const int wm = ell_pad <= 24 ? 1 : 2;
+    const int wn = kWarps / wm;
+    int options[3];
+    int nopt = 0;
+    if (wm == 1 || ell_pad >= 64) {
+        options[0] = 2, options[1] = 1, nopt = 2;
+    } else {
+        options[0] = 4, options[1] = 2, options[2] = 1, nopt = 3;
+    }
     // column tile: least padded work; ties -> wider tile (fewer Omega regenerations)
-    int best_nw = 1;
+    int best_nw = options[0];
     int64_t best_cols = INT64_MAX;
-    for (int nw : {4, 2, 1}) {
-        if (nw == 4 && mt > 8) continue;
-        const int64_t nt = kWarps * 8 * nw;
+    for (int i = 0; i < nopt; ++i) {
+        const int64_t nt = 8LL * options[i] * wn;
         const int64_t cols = ((n + nt - 1) / nt) * nt;
         if (cols < best_cols) {
             best_cols = cols;
-            best_nw = nw;
+            best_nw = options[i];
         }
     }
-    plan->mt = mt;
+    plan->ell_pad = ell_pad;
+    plan->mt = ell_pad / 8;
     plan->nw = best_nw;
-    plan->nt = kWarps * 8 * best_nw;
+    plan->nt = 8 * best_nw * wn;
     plan->ntiles_col = (n + plan->nt - 1) / plan->nt;
     plan->nchunk = (m + kKc - 1) / kKc;
     plan->total_chunks = batch * plan->ntiles_col * plan->nchunk;
@@ -364,20 +383,23 @@ bool sketch_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int num_
     plan->grid = static_cast<int>(grid);
     const int64_t per = (plan->total_chunks + grid - 1) / grid;
     plan->max_segs = static_cast<int>(per / plan->nchunk + 2);
-    plan->smem = smem_for(mt, best_nw);
-    plan->partial_elems = static_cast<size_t>(grid) * plan->max_segs * (8 * mt) * plan->nt;
+    const int sbytes = (plan->nt + ell_pad) * kKc * 8;
+    int stages = kStageBudget / sbytes;
+    if (stages > 8) stages = 8;
+    plan->smem = 1024 + static_cast<size_t>(stages) * sbytes + 24 * stages;
+    plan->partial_elems = static_cast<size_t>(grid) * plan->max_segs * ell_pad * plan->nt;
     return true;
 }
 
 cudaError_t launch_sketch(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap,
                           cudaStream_t stream) {
-    return p.omega_mode == 1 ? launch_mt<1>(p, plan, tmap, stream)
-                             : launch_mt<0>(p, plan, tmap, stream);
+    return p.omega_mode == 1 ? launch_mode<1>(p, plan, tmap, stream)
+                             : launch_mode<0>(p, plan, tmap, stream);
 }
 
 cudaError_t launch_philox_omega(uint64_t seed, int64_t s, int64_t ell, int64_t m, double* out,
                                 int64_t ldo, cudaStream_t stream) {
-    const int64_t total = ((ell + 3) / 4) * m;
+    const int64_t total = ((m + 3) / 4) * ell;
     int64_t blocks = (total + 255) / 256;
     if (blocks > 4096) blocks = 4096;
     philox_omega_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(seed, s, ell, m, out, ldo);

@@ -183,25 +183,29 @@ class Engine:
 
     # ---- end to end from host buffers ------------------------------------------
     def compress_host(self, a_host: torch.Tensor, ell: int, rule: RankRule, *, seed=0,
-                      subdomain_base=0, group=8, want_skel=True, verify=False):
+                      subdomain_base=0, group=8, want_skel=True, verify=False, out=None):
         """spidgpu_compress_host: host (pinned) A in, host factors out; the
-        H2D/D2H copies are inside the call, overlapped with compute."""
+        H2D/D2H copies are inside the call, overlapped with compute. `out`
+        may pass preallocated (pinned) host tensors keyed like the result."""
         S, n, m = a_host.shape
         kcap = rule.cap(ell, n)
-        out = {
-            "indices": np.zeros((S, kcap), dtype=np.int64),
-            "coeffs": np.zeros((S, n, kcap), dtype=np.float64),
-            "rank": np.zeros(S, dtype=np.int64),
-            "residual_fro": np.zeros(S, dtype=np.float64),
-            "status": np.zeros(S, dtype=np.int32),
-        }
-        if want_skel:
-            out["skel"] = np.empty((S, kcap, m), dtype=np.float64)
-        if verify:
-            out["err2"] = np.zeros(S, dtype=np.float64)
-            out["ref2"] = np.zeros(S, dtype=np.float64)
+        if out is None:
+            pin = a_host.is_pinned()
+            mk = lambda shape, dt: torch.zeros(shape, dtype=dt, pin_memory=pin)  # noqa: E731
+            out = {
+                "indices": mk((S, kcap), torch.int64),
+                "coeffs": mk((S, n, kcap), torch.float64),
+                "rank": mk((S,), torch.int64),
+                "residual_fro": mk((S,), torch.float64),
+                "status": mk((S,), torch.int32),
+            }
+            if want_skel:
+                out["skel"] = mk((S, kcap, m), torch.float64)
+            if verify:
+                out["err2"] = mk((S,), torch.float64)
+                out["ref2"] = mk((S,), torch.float64)
         om = self.omega(seed, subdomain_base)
-        g = lambda k: C.c_void_p(out[k].ctypes.data) if k in out else None  # noqa: E731
+        g = lambda k: C.c_void_p(out[k].data_ptr()) if k in out else None  # noqa: E731
         self.h.check(N.lib.spidgpu_compress_host(
             self.h.h, C.c_void_p(a_host.data_ptr()), m, n, S, ell, C.byref(om), C.byref(rule.c()),
             kcap, group, g("indices"), g("coeffs"), g("skel"), g("rank"), g("residual_fro"),
