@@ -56,11 +56,11 @@ struct DevBuf {
 
 // One workspace set per concurrently used stream.
 struct Workspace {
-    DevBuf partial, rws, wws, ybuf, vpart, flag;
+    DevBuf partial, rws, wws, r11ws, ybuf, vpart, flag;
     // host-API / compress_host staging
     DevBuf a, omega, idx, coeffs, skel, rank, resid, status, err2, ref2, rows, out, pivots, r, q;
     void release() {
-        for (DevBuf* b : {&partial, &rws, &wws, &ybuf, &vpart, &flag, &a, &omega, &idx, &coeffs,
+        for (DevBuf* b : {&partial, &rws, &wws, &r11ws, &ybuf, &vpart, &flag, &a, &omega, &idx, &coeffs,
                           &skel, &rank, &resid, &status, &err2, &ref2, &rows, &out, &pivots, &r,
                           &q})
             b->release();
@@ -233,10 +233,13 @@ int do_cpqr(spidgpu_handle h, Workspace& ws, const double* Y, int64_t rows, int6
         return fail(h, SPID_SHAPE_UNSUPPORTED, "matrix too large for the CPQR kernel");
     RuleInfo ri = resolve_rule(rule, rows, n, kcap);
     if (ri.status) return fail(h, ri.status, "rank rule");
-    const bool w_smem = cpqr_smem_bytes(rows, n, true) <= cpqr_max_dyn_smem();
     const int64_t step_cap = std::max<int64_t>(1, ri.step_limit);
+    const bool w_smem = cpqr_smem_bytes(rows, n, step_cap, true) <= cpqr_max_dyn_smem();
     CK(h, ws.rws.ensure(sizeof(double) * batch * step_cap * n, st));
-    if (!w_smem) CK(h, ws.wws.ensure(sizeof(double) * batch * rows * n, st));
+    if (!w_smem) {
+        CK(h, ws.wws.ensure(sizeof(double) * batch * rows * n, st));
+        CK(h, ws.r11ws.ensure(sizeof(double) * batch * step_cap * step_cap, st));
+    }
     CpqrParams p{};
     p.Y = Y;
     p.rows = rows;
@@ -255,6 +258,7 @@ int do_cpqr(spidgpu_handle h, Workspace& ws, const double* Y, int64_t rows, int6
     p.npad = static_cast<int>(n);
     p.w_ws = ws.wws.as<double>();
     p.r_ws = ws.rws.as<double>();
+    p.r11_ws = ws.r11ws.as<double>();
     p.indices = indices;
     p.C = C;
     p.strideC = strideC;
@@ -302,11 +306,41 @@ int do_verify(spidgpu_handle h, Workspace& ws, const double* A, int64_t m, int64
     p.kcap = kcap;
     p.strideC = strideC;
     p.rank = rank;
-    p.nblk = verify_row_blocks(m);
-    CK(h, ws.vpart.ensure(sizeof(double) * 2 * batch * p.nblk, st));
-    p.part = ws.vpart.as<double>();
     p.err2 = err2;
     p.ref2 = ref2;
+    // TMA path: both operands need 16-byte aligned bases and even leading dims
+    const bool tma_ok = (lda % 2 == 0) && (strideA % 2 == 0) && (ldskel % 2 == 0) &&
+                        (strideS % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
+                        (reinterpret_cast<uintptr_t>(skel) % 16 == 0) && kcap >= 1;
+    VerifyPlan plan;
+    if (tma_ok && verify_make_plan(m, n, batch, kcap, h->num_sms, &plan)) {
+        CUtensorMap tA, tS;
+        cuuint32_t estr[3] = {1, 1, 1};
+        cuuint64_t gA[3] = {static_cast<cuuint64_t>(m), static_cast<cuuint64_t>(n),
+                            static_cast<cuuint64_t>(batch)};
+        cuuint64_t sA[2] = {static_cast<cuuint64_t>(lda) * 8, static_cast<cuuint64_t>(strideA) * 8};
+        cuuint32_t bA[3] = {16, static_cast<cuuint32_t>(plan.nt), 1};
+        cuuint64_t gS[3] = {static_cast<cuuint64_t>(m), static_cast<cuuint64_t>(kcap),
+                            static_cast<cuuint64_t>(batch)};
+        cuuint64_t sS[2] = {static_cast<cuuint64_t>(ldskel) * 8, static_cast<cuuint64_t>(strideS) * 8};
+        cuuint32_t bS[3] = {16, static_cast<cuuint32_t>(4 * plan.ks), 1};
+        CUresult c1 = h->encode(&tA, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(A), gA,
+                                sA, bA, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        CUresult c2 = h->encode(&tS, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(skel),
+                                gS, sS, bS, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (c1 == CUDA_SUCCESS && c2 == CUDA_SUCCESS) {
+            CK(h, ws.vpart.ensure(sizeof(double) * plan.part_elems, st));
+            CK(h, launch_verify_tma(p, plan, &tA, &tS, ws.vpart.as<double>(), st));
+            h->launches += 2;
+            return SPID_OK;
+        }
+    }
+    p.nblk = verify_row_blocks(m);  // generic slab path (odd leading dims, unaligned bases)
+    CK(h, ws.vpart.ensure(sizeof(double) * 2 * batch * p.nblk, st));
+    p.part = ws.vpart.as<double>();
     CK(h, launch_verify(p, h->num_sms, st));
     h->launches += 2;
     return SPID_OK;

@@ -60,6 +60,8 @@ __global__ void __launch_bounds__(kCpqrThreads)
     double* colsq;
     int* perm;
     int* posof;
+    double* diag;  // R(t,t) in selection order (step_cap)
+    double* r11;   // R11 in position order, rank x rank row-major (step_cap^2)
     {
         unsigned char* cur = smem_raw;
         if (kWInShared) {
@@ -75,6 +77,15 @@ __global__ void __launch_bounds__(kCpqrThreads)
         perm = reinterpret_cast<int*>(cur);
         cur += sizeof(int) * n;
         posof = reinterpret_cast<int*>(cur);
+        cur += sizeof(int) * n;
+        cur = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(cur) + 15) & ~uintptr_t(15));
+        diag = reinterpret_cast<double*>(cur);
+        cur += sizeof(double) * p.step_cap;
+        if (kWInShared) {
+            r11 = reinterpret_cast<double*>(cur);
+        } else {
+            r11 = p.r11_ws + static_cast<size_t>(b) * p.step_cap * p.step_cap;
+        }
     }
     double* R = p.r_ws + static_cast<size_t>(b) * p.step_cap * n;  // R[s][col]
     const double* Y = p.Y + static_cast<size_t>(b) * p.strideY;
@@ -113,6 +124,7 @@ __global__ void __launch_bounds__(kCpqrThreads)
     double lmax = 0.0;
     for (int j = tid; j < n; j += kCpqrThreads) {
         double s = 0.0;
+#pragma unroll 8
         for (int i = 0; i < rows; ++i) {
             const double w = W[i * npad + j];
             s = add_rn(s, mul_rn(w, w));
@@ -190,6 +202,7 @@ __global__ void __launch_bounds__(kCpqrThreads)
                 posof[ix] = s;
                 posof[cs] = ps;
                 R[static_cast<size_t>(s) * n + ix] = v;  // R(s,s) = ||w_s|| (qr.cpp:89-90)
+                diag[s] = v;
             }
             sh.best_v = v;
             sh.best_i = ix;
@@ -213,8 +226,10 @@ __global__ void __launch_bounds__(kCpqrThreads)
         for (int j = tid; j < n; j += kCpqrThreads) {
             if (posof[j] <= s) continue;
             double r1 = 0.0;
+#pragma unroll 8
             for (int i = 0; i < rows; ++i) r1 = add_rn(r1, mul_rn(W[i * npad + pc], W[i * npad + j]));
             double r2 = 0.0;
+#pragma unroll 8
             for (int i = 0; i < rows; ++i) {
                 const double q = W[i * npad + pc];
                 const double w = sub_rn(W[i * npad + j], mul_rn(r1, q));
@@ -222,6 +237,7 @@ __global__ void __launch_bounds__(kCpqrThreads)
                 r2 = add_rn(r2, mul_rn(q, w));
             }
             double nn = 0.0;
+#pragma unroll 8
             for (int i = 0; i < rows; ++i) {
                 const double w = sub_rn(W[i * npad + j], mul_rn(r2, W[i * npad + pc]));
                 W[i * npad + j] = w;
@@ -247,13 +263,20 @@ __global__ void __launch_bounds__(kCpqrThreads)
         }
         p.resid[b] = sqrt(rsq);
         double max_diag = 0.0;  // qr.cpp:135-140
-        for (int t = 0; t < rank; ++t)
-            max_diag = fmax(max_diag, fabs(R[static_cast<size_t>(t) * n + perm[t]]));
+        for (int t = 0; t < rank; ++t) max_diag = fmax(max_diag, fabs(diag[t]));
         int sing = 0;
         for (int t = 0; t < rank; ++t)
-            if (fabs(R[static_cast<size_t>(t) * n + perm[t]]) < 1e-14 * max_diag || max_diag == 0.0)
-                sing = 1;
+            if (fabs(diag[t]) < 1e-14 * max_diag || max_diag == 0.0) sing = 1;
         sh.flag = sing;
+    }
+    // Q (= the normalised pivot columns kept in W) must be read out before W's
+    // space is reused for the solve vectors
+    if (p.Qout) {
+        double* Qo = p.Qout + static_cast<size_t>(b) * rows * p.kcap;
+        for (int e = tid; e < rank * rows; e += kCpqrThreads) {
+            const int i = e % rows, t = e / rows;
+            Qo[static_cast<size_t>(t) * rows + i] = W[i * npad + perm[t]];
+        }
     }
     __syncthreads();
     if (sh.flag && rank < n) {
@@ -262,6 +285,18 @@ __global__ void __launch_bounds__(kCpqrThreads)
     }
 
     // ---- coefficients in source column order (id.cpp:9-28) ----------------
+    // R11 (position order) into r11[]; each non-skeleton column's right-hand
+    // side R(0:rank, j) into X[t][j] (W's space, thread-contiguous); then the
+    // back substitution of qr.cpp:143-149 runs in place, same operation order.
+    double* X = W;
+    for (int e = tid; e < rank * rank; e += kCpqrThreads) {
+        const int ii = e / rank, jj = e % rank;
+        r11[e] = jj >= ii ? R[static_cast<size_t>(ii) * n + perm[jj]] : 0.0;
+    }
+    for (int j = tid; j < n; j += kCpqrThreads)
+        if (posof[j] >= rank)
+            for (int t = 0; t < rank; ++t) X[t * npad + j] = R[static_cast<size_t>(t) * n + j];
+    __syncthreads();
     double* C = p.C + static_cast<size_t>(b) * p.strideC;
     const int kcap = static_cast<int>(p.kcap);
     int nonfinite = 0;
@@ -272,15 +307,16 @@ __global__ void __launch_bounds__(kCpqrThreads)
             for (int i = 0; i < rank; ++i) cj[i] = (i == pj) ? 1.0 : 0.0;
             continue;
         }
-        // back substitution R11 x = R(:, j) (qr.cpp:143-149), x kept in C
         for (int ii = rank - 1; ii >= 0; --ii) {
-            double sum = R[static_cast<size_t>(ii) * n + j];
-            for (int jj = ii + 1; jj < rank; ++jj)
-                sum = sub_rn(sum, mul_rn(R[static_cast<size_t>(ii) * n + perm[jj]], cj[jj]));
-            const double x = div_rn(sum, R[static_cast<size_t>(ii) * n + perm[ii]]);
-            cj[ii] = x;
+            double sum = X[ii * npad + j];
+            const double* rrow = r11 + ii * rank;
+#pragma unroll 4
+            for (int jj = ii + 1; jj < rank; ++jj) sum = sub_rn(sum, mul_rn(rrow[jj], X[jj * npad + j]));
+            const double x = div_rn(sum, rrow[ii]);
+            X[ii * npad + j] = x;
             nonfinite |= !isfinite(x);
         }
+        for (int i = 0; i < rank; ++i) cj[i] = X[i * npad + j];
     }
     nonfinite = __syncthreads_or(nonfinite);
     if (nonfinite) {  // id.cpp:25-26
@@ -301,13 +337,6 @@ __global__ void __launch_bounds__(kCpqrThreads)
                 pos < i ? 0.0 : R[static_cast<size_t>(i) * n + perm[pos]];
         }
     }
-    if (p.Qout) {
-        double* Qo = p.Qout + static_cast<size_t>(b) * rows * kcap;
-        for (int e = tid; e < rank * rows; e += kCpqrThreads) {
-            const int i = e % rows, t = e / rows;
-            Qo[static_cast<size_t>(t) * rows + i] = W[i * npad + perm[t]];
-        }
-    }
     if (tid == 0) {
         p.rank[b] = rank;
         p.status[b] = SPID_OK;
@@ -316,16 +345,16 @@ __global__ void __launch_bounds__(kCpqrThreads)
 
 }  // namespace
 
-size_t cpqr_smem_bytes(int64_t rows, int64_t n, bool w_in_shared) {
-    size_t bytes = 2 * sizeof(double) * n + 2 * sizeof(int) * n;
-    if (w_in_shared) bytes += sizeof(double) * rows * n;
+size_t cpqr_smem_bytes(int64_t rows, int64_t n, int64_t step_cap, bool w_in_shared) {
+    size_t bytes = 2 * sizeof(double) * n + 2 * sizeof(int) * n + 16 + sizeof(double) * step_cap;
+    if (w_in_shared) bytes += sizeof(double) * (rows * n + step_cap * step_cap);
     return bytes;
 }
 
 size_t cpqr_max_dyn_smem() { return 200 * 1024; }
 
 cudaError_t launch_cpqr(const CpqrParams& p, bool w_in_shared, cudaStream_t stream) {
-    const size_t smem = cpqr_smem_bytes(p.rows, p.n, w_in_shared);
+    const size_t smem = cpqr_smem_bytes(p.rows, p.n, p.step_cap, w_in_shared);
     if (w_in_shared) {
         if (smem > 48 * 1024) {
             cudaError_t e = cudaFuncSetAttribute(cpqr_id_kernel<true>,

@@ -24,6 +24,7 @@ struct CpqrParams {
     int npad;
     double* w_ws;        // rows*npad per subdomain when W does not fit smem
     double* r_ws;        // step_cap*n per subdomain
+    double* r11_ws;      // step_cap^2 per subdomain when R11 does not fit smem
     int64_t* indices;
     double* C;
     int64_t strideC;
@@ -34,7 +35,7 @@ struct CpqrParams {
     double* Rout;
     double* Qout;
 };
-size_t cpqr_smem_bytes(int64_t rows, int64_t n, bool w_in_shared);
+size_t cpqr_smem_bytes(int64_t rows, int64_t n, int64_t step_cap, bool w_in_shared);
 size_t cpqr_max_dyn_smem();
 cudaError_t launch_cpqr(const CpqrParams& p, bool w_in_shared, cudaStream_t stream);
 
@@ -98,6 +99,16 @@ struct VerifyParams {
     double* ref2;
 };
 int64_t verify_row_blocks(int64_t m);
+struct VerifyPlan {
+    int nwv, ks, nt;
+    int64_t ntiles_col, nchunk, total_chunks;
+    int grid, max_segs;
+    size_t part_elems;
+};
+bool verify_make_plan(int64_t m, int64_t n, int64_t batch, int64_t kcap, int num_sms,
+                      VerifyPlan* plan);
+cudaError_t launch_verify_tma(const VerifyParams& p, const VerifyPlan& plan, const CUtensorMap* tA,
+                              const CUtensorMap* tS, double* part, cudaStream_t stream);
 cudaError_t launch_verify(const VerifyParams& p, int num_sms, cudaStream_t stream);
 cudaError_t launch_reconstruct(const double* skel, int64_t m, int64_t ldskel, int64_t strideS,
                                const double* C, int64_t kcap, int64_t strideC,
