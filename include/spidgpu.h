@@ -80,6 +80,12 @@ const char* spidgpu_last_error(spidgpu_handle h);
 int spidgpu_abi_version(void);
 /* Kernel launches issued through this handle since creation (instrumentation). */
 int64_t spidgpu_launch_count(spidgpu_handle h);
+/* Handle options. SPIDGPU_OPT_GENERIC_CPQR = 1 routes column IDs of
+ * sketch-sized matrices through the general (shared/global-memory) CPQR
+ * kernel instead of the register-resident one; both are bit-exact with the
+ * reference, the option exists so tests can cover both. */
+#define SPIDGPU_OPT_GENERIC_CPQR 1
+int spidgpu_set_option(spidgpu_handle h, int option, int64_t value);
 
 /* =====================================================================
  * Batched device API (the hot path). Subdomain s of a batch lives at

@@ -7,7 +7,17 @@ verification, all in libspidgpu.so behind the C ABI in include/spidgpu.h.
 
     from paper_2103_01380_b200 import spid       # reference-facing API
     from paper_2103_01380_b200.engine import Engine  # batched device API
+
+The native library is loaded on first use of any submodule that needs it
+(_native raises ImportError if it is not built -- there is no CPU fallback).
 """
-from ._native import SpidError  # noqa: F401  (fails loudly if the .so is missing)
 
 __all__ = ["SpidError"]
+
+
+def __getattr__(name):
+    if name == "SpidError":
+        from ._native import SpidError
+
+        return SpidError
+    raise AttributeError(name)

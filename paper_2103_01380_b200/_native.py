@@ -18,6 +18,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "spidgpu.h")
 RULE_FIXED, RULE_TOL, RULE_BLOCKED = 0, 1, 2
 OMEGA_EXPLICIT, OMEGA_PHILOX = 0, 1
 FIELD_TGV4, FIELD_TGV5, FIELD_MULTIMODE = 0, 1, 2
+SPIDGPU_OPT_GENERIC_CPQR = 1
 
 
 class SpidError(RuntimeError):
@@ -62,6 +63,7 @@ _SIGS = {
     "spidgpu_last_error": (C.c_char_p, [_H]),
     "spidgpu_abi_version": (C.c_int, []),
     "spidgpu_launch_count": (C.c_int64, [_H]),
+    "spidgpu_set_option": (C.c_int, [_H, C.c_int, C.c_int64]),
     "spidgpu_sketch_batched": (C.c_int, [_H, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _OM, _vp,
                                          _i64, _i64, _vp]),
     "spidgpu_philox_omega": (C.c_int, [_H, C.c_uint64, _i64, _i64, _i64, _vp, _i64, _vp]),

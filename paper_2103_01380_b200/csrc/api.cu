@@ -83,6 +83,7 @@ struct spidgpu_context {
     EncodeTiledFn encode = nullptr;
     int64_t launches = 0;
     std::string last_error;
+    bool force_generic_cpqr = false;  // tests: exercise the shared/global-W kernel too
 };
 
 namespace {
@@ -234,9 +235,10 @@ int do_cpqr(spidgpu_handle h, Workspace& ws, const double* Y, int64_t rows, int6
     RuleInfo ri = resolve_rule(rule, rows, n, kcap);
     if (ri.status) return fail(h, ri.status, "rank rule");
     const int64_t step_cap = std::max<int64_t>(1, ri.step_limit);
+    const bool reg = cpqr_reg_supported(rows, n, step_cap) && !h->force_generic_cpqr;
     const bool w_smem = cpqr_smem_bytes(rows, n, step_cap, true) <= cpqr_max_dyn_smem();
     CK(h, ws.rws.ensure(sizeof(double) * batch * step_cap * n, st));
-    if (!w_smem) {
+    if (!reg && !w_smem) {
         CK(h, ws.wws.ensure(sizeof(double) * batch * rows * n, st));
         CK(h, ws.r11ws.ensure(sizeof(double) * batch * step_cap * step_cap, st));
     }
@@ -268,7 +270,10 @@ int do_cpqr(spidgpu_handle h, Workspace& ws, const double* Y, int64_t rows, int6
     p.pivots = pivots;
     p.Rout = R;
     p.Qout = Q;
-    CK(h, launch_cpqr(p, w_smem, st));
+    if (reg)
+        CK(h, launch_cpqr_reg(p, st));
+    else
+        CK(h, launch_cpqr(p, w_smem, st));
     h->launches += 1;
     return SPID_OK;
 }
@@ -548,6 +553,14 @@ int spidgpu_destroy(spidgpu_handle h) {
 const char* spidgpu_last_error(spidgpu_handle h) { return h ? h->last_error.c_str() : ""; }
 
 int64_t spidgpu_launch_count(spidgpu_handle h) { return h ? h->launches : 0; }
+
+int spidgpu_set_option(spidgpu_handle h, int option, int64_t value) {
+    if (!h) return SPID_INVALID_ARGUMENT;
+    switch (option) {
+        case SPIDGPU_OPT_GENERIC_CPQR: h->force_generic_cpqr = value != 0; return SPID_OK;
+        default: return SPID_INVALID_ARGUMENT;
+    }
+}
 
 // ---- batched device API ----------------------------------------------------------
 int spidgpu_sketch_batched(spidgpu_handle h, const double* A, int64_t m, int64_t n, int64_t lda,

@@ -38,6 +38,9 @@ struct CpqrParams {
 size_t cpqr_smem_bytes(int64_t rows, int64_t n, int64_t step_cap, bool w_in_shared);
 size_t cpqr_max_dyn_smem();
 cudaError_t launch_cpqr(const CpqrParams& p, bool w_in_shared, cudaStream_t stream);
+// register-resident variant for sketch-sized inputs (rows <= 80, n <= 512)
+bool cpqr_reg_supported(int64_t rows, int64_t n, int64_t step_cap);
+cudaError_t launch_cpqr_reg(const CpqrParams& p, cudaStream_t stream);
 
 // ---- sketch Y = Omega * A (sketch.cu) -------------------------------------
 struct SketchPlan {

@@ -256,3 +256,29 @@ def test_determinism_bitwise(spid, orc):
     a = orc.seeded_matrix(20, 12, 77)
     q1, q2 = spid.qr(a, rank=6), spid.qr(a, rank=6)
     assert _eq(q1["pivots"], q2["pivots"]) and _eq(q1["q"], q2["q"]) and _eq(q1["r"], q2["r"])
+
+
+@pytest.mark.parametrize("m,n,k", [(48, 256, 32), (30, 512, 20), (80, 256, 64), (20, 100, 10),
+                                   (7, 300, 5), (33, 17, 17)])
+def test_both_cpqr_kernels_bitwise(spid, orc, m, n, k):
+    """Register-resident and shared/global-W CPQR kernels both reproduce the
+    reference bit for bit (SPIDGPU_OPT_GENERIC_CPQR switches between them)."""
+    from paper_2103_01380_b200 import _native as N
+
+    h = N.handle(0)
+    a = orc.seeded_matrix(m, n, 77 + m + n)
+    o = orc.column_id(a, rank=k)
+    ot = orc.column_id(a, tol=1e-3)
+    try:
+        for generic in (0, 1):
+            h.check(N.lib.spidgpu_set_option(h.h, N.SPIDGPU_OPT_GENERIC_CPQR, generic))
+            g = spid.column_id(a, rank=k)
+            assert _eq(g.skeleton_indices, o.indices) and _eq(g.coeffs, o.coeffs), generic
+            assert g.qr_residual_fro == o.residual_fro
+            gt = spid.column_id(a, tol=1e-3)
+            assert _eq(gt.coeffs, ot.coeffs) and gt.achieved_rank == ot.rank
+            q = spid.qr(a, rank=k)
+            qo = orc.qr(a, rank=k)
+            assert _eq(q["q"], qo.q) and _eq(q["r"], qo.r) and _eq(q["pivots"], qo.pivots)
+    finally:
+        N.lib.spidgpu_set_option(h.h, N.SPIDGPU_OPT_GENERIC_CPQR, 0)
