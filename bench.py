@@ -280,14 +280,18 @@ def run_ours(args):
     raw_total = raw_local * world  # weak scaling: equal share per rank
     value = raw_total / (ms_step / 1e3) / 1e9
 
-    # verify phase (timed separately) and the report
+    # verify phase (timed separately, after one untimed call that sizes its
+    # workspace) and the report
+    eng.verify(A, res)
     torch.cuda.synchronize()
     v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nv = 3
     v0.record(stream)
-    err2, ref2 = eng.verify(A, res)
+    for _ in range(nv):
+        err2, ref2 = eng.verify(A, res)
     v1.record(stream)
     torch.cuda.synchronize()
-    verify_ms = v0.elapsed_time(v1)
+    verify_ms = v0.elapsed_time(v1) / nv
     sums = D.local_sums(err2.cpu(), ref2.cpu(), res.rank.cpu(), cfg.m, cfg.n).to(dev)
     report = D.reduce_report(sums)
     vt = torch.tensor([verify_ms], dtype=torch.float64, device=dev)

@@ -166,6 +166,58 @@ int spidgpu_compress_batched(spidgpu_handle h, const double* A, int64_t m, int64
                              void* stream);
 
 /* =====================================================================
+ * SPID proper: coarse-grid skeleton + multilinear lift
+ * (SubsampleSpec / InterpOperator, proj/include/spid/grid.hpp:188-208,
+ * proj/include/spid/interp.hpp:14-53).
+ * ===================================================================== */
+
+/* A strided structured SubsampleSpec (proj/src/grid.cpp:62-75) on a 1-3 axis
+ * grid, optionally repeated over `nqoi` QoI blocks stacked along the rows
+ * (row = q * P + p; nqoi = 1 is the reference's single-QoI layout). */
+typedef struct spidgpu_grid_spec {
+    int32_t naxes;            /* 1..3                                           */
+    int32_t include_boundary; /* pin the last point of non-periodic axes        */
+    int64_t dims[3];          /* points per axis (axis 0 fastest)               */
+    int64_t strides[3];       /* >= 1                                           */
+    int32_t periodic[3];
+    int32_t nqoi;             /* >= 1                                           */
+} spidgpu_grid_spec;
+
+/* SubsampleSpec::row_indices (proj/src/grid.cpp:108-130), repeated per QoI
+ * block. Writes min(count, cap) entries; *count = |J|. Pure index arithmetic. */
+int spidgpu_row_indices(const spidgpu_grid_spec* spec, int64_t* rows, int64_t cap, int64_t* count);
+
+/* spid::spid (proj/src/id.cpp:62-83): sketch B = A(J, :), column ID of B,
+ * skeleton kept on the COARSE rows (B(:, I), |J| x kcap, ld |J|). */
+int spidgpu_spid(spidgpu_handle h, const double* a, int64_t m, int64_t n,
+                 const spidgpu_grid_spec* spec, const spidgpu_rank_rule* rule, int64_t kcap,
+                 int64_t* indices, double* coeffs, double* coarse_skeleton, int64_t* rank,
+                 double* residual_fro);
+
+/* InterpOperator::apply (proj/src/interp.cpp:168-186), host buffers:
+ * fine (m x k, m = P*nqoi) = M * coarse (|J| x k). Bit-identical to the
+ * reference operator built by InterpOperator::from_spec. */
+int spidgpu_interp_apply(spidgpu_handle h, const spidgpu_grid_spec* spec, const double* coarse,
+                         int64_t k, double* fine);
+
+/* spid::reconstruct(SpidFactors) (proj/src/id.cpp:92-96): M * skel_c * C. */
+int spidgpu_spid_reconstruct(spidgpu_handle h, const spidgpu_grid_spec* spec,
+                             const double* coarse_skeleton, int64_t k, const double* coeffs,
+                             int64_t n, double* out);
+
+/* Batched device forms. gather: skel_c_s(:, t) = A_s(J, I_s[t]);
+ * lift: fine_s(:, t) = M * coarse_s(:, t) for t < rank[s]. */
+int spidgpu_gather_coarse_batched(spidgpu_handle h, const double* A, int64_t m, int64_t n,
+                                  int64_t lda, int64_t strideA, int64_t batch,
+                                  const spidgpu_grid_spec* spec, const int64_t* indices,
+                                  int64_t kcap, const int64_t* rank, double* skel_c,
+                                  int64_t ldskel, int64_t strideS, void* stream);
+int spidgpu_interp_apply_batched(spidgpu_handle h, const spidgpu_grid_spec* spec,
+                                 const double* coarse, int64_t ldc, int64_t strideC, int64_t k,
+                                 const int64_t* rank, int64_t batch, double* fine, int64_t ldf,
+                                 int64_t strideF, void* stream);
+
+/* =====================================================================
  * Host-buffer API: one call per reference function (synchronous).
  * ===================================================================== */
 

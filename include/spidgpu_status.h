@@ -28,6 +28,8 @@ enum spidgpu_status {
     SPID_ZERO_DENOMINATOR = 13, /* "ZeroDenominator"  metrics.cpp:6-9 */
     SPID_BAD_SUBSAMPLE_SPEC = 14,/* "BadSubsampleSpec" grid.cpp:65-69 */
     SPID_EMPTY_SKETCH = 15,     /* "EmptySketch"      grid.cpp:78,110 */
+    SPID_EXTRAPOLATION_REQUIRED = 16, /* "ExtrapolationRequired" interp.cpp:27-29 */
+    SPID_BAD_GRID_GEOM = 17,    /* "BadGridGeom"      grid.cpp:8-14 */
     /* codes that exist only on the device path */
     SPID_CUDA_ERROR = 100,      /* "CudaError" */
     SPID_INVALID_ARGUMENT = 101,/* "InvalidArgument" (null pointer, bad leading dim) */

@@ -34,7 +34,7 @@ STATUS_NAMES = {
     4: "SingularPivot", 5: "DimensionMismatch", 6: "NonFiniteCoeffs",
     7: "BadRankRule", 8: "EmptyMatrix", 9: "EmptySelection",
     10: "IndexOutOfRange", 11: "GeometryMismatch", 12: "ZeroReference",
-    13: "ZeroDenominator", 14: "BadSubsampleSpec", 15: "EmptySketch",
+    13: "ZeroDenominator", 14: "BadSubsampleSpec", 15: "EmptySketch", 16: "ExtrapolationRequired", 17: "BadGridGeom",
     100: "CudaError", 101: "InvalidArgument", 102: "ShapeUnsupported", 103: "NoDevice",
 }
 
@@ -126,7 +126,34 @@ class _Port:
         L.orc_error_terms.argtypes = [_D, _sz, _sz, _D, _sz, _D, _sz, _sz, _D, _D]
         L.orc_rel_frob_error.argtypes = [_D, _D, _sz, _D]
         L.orc_compression_factor.argtypes = [_sz, _sz, _sz, _D]
+        L.orc_row_indices.argtypes = [_SZ, C.POINTER(C.c_int), _SZ, _sz, C.c_int, _I64, _sz, _SZ]
+        L.orc_interp_apply.argtypes = [_SZ, C.POINTER(C.c_int), _SZ, _sz, C.c_int, _D, _sz, _D]
         self.lib = L
+
+    @staticmethod
+    def _spec(dims, strides, periodic):
+        nax = len(dims)
+        return ((C.c_size_t * nax)(*dims), (C.c_int * nax)(*([int(bool(x)) for x in periodic]
+                                                               if periodic else [0] * nax)),
+                (C.c_size_t * nax)(*strides), nax)
+
+    def row_indices(self, dims, strides, periodic=None, include_boundary=True):
+        d, p, s, nax = self._spec(dims, strides, periodic)
+        cap = int(np.prod(dims))
+        out = np.zeros(cap, dtype=np.int64)
+        cnt = C.c_size_t(0)
+        self._check(self.lib.orc_row_indices(d, p, s, nax, int(include_boundary), _ip(out), cap,
+                                             C.byref(cnt)))
+        return out[:cnt.value].copy()
+
+    def interp_apply(self, dims, strides, coarse, periodic=None, include_boundary=True):
+        """InterpOperator::from_spec(spec).apply(coarse) (interp.cpp:45-100, 168-186)."""
+        d, p, s, nax = self._spec(dims, strides, periodic)
+        coarse = _f64(coarse)
+        fine = np.zeros((int(np.prod(dims)), coarse.shape[1]), order="F")
+        self._check(self.lib.orc_interp_apply(d, p, s, nax, int(include_boundary), _dp(coarse),
+                                              coarse.shape[1], _dp(fine)))
+        return fine
 
     @staticmethod
     def _check(st):
@@ -274,7 +301,41 @@ class _Ref:
         L.ref_compression_factor.argtypes = [_sz, _sz, _sz, _D, cp, _sz]
         L.ref_compress_batch.argtypes = [_D, _sz, _sz, _sz, _D, _sz, _sz, C.c_int, _SZ, _D, cp,
                                          _sz]
+        L.ref_spid.argtypes = [_D, _sz, _sz, _SZ, C.POINTER(C.c_int), _SZ, _sz, C.c_int, C.c_int,
+                               _sz, C.c_double, _sz, _I64, _D, _D, _D, _SZ, _D, cp, _sz]
+        L.ref_interp_apply.argtypes = [_SZ, C.POINTER(C.c_int), _SZ, _sz, C.c_int, _D, _sz, _D,
+                                       cp, _sz]
         self.lib = L
+
+    def spid(self, a, dims, strides, rank=None, tol=None, periodic=None, include_boundary=True):
+        """spid::spid + reconstruct(SpidFactors) (proj/src/id.cpp:62-96): IdResult
+        with the COARSE skeleton; .y holds the reconstruction."""
+        a = _f64(a)
+        m, n = a.shape
+        mode, k, t, _ = _rule_args(rank, tol)
+        d, p, s, nax = _Port._spec(dims, strides, periodic)
+        kcap = max(1, min(m, n))
+        mc = m  # upper bound for the coarse rows
+        idx = np.zeros(kcap, dtype=np.int64)
+        coeffs = np.zeros((kcap, n), order="F")
+        skel = np.zeros((mc * kcap,))
+        approx = np.zeros((m, n), order="F")
+        rk, res = C.c_size_t(0), C.c_double(0)
+        self._call(self.lib.ref_spid, _dp(a), m, n, d, p, s, nax, int(include_boundary), mode, k,
+                   t, kcap, _ip(idx), _dp(coeffs), _dp(skel), _dp(approx), C.byref(rk),
+                   C.byref(res))
+        k_ = rk.value
+        rows = len(port().row_indices(dims, strides, periodic, include_boundary))
+        sk = np.asfortranarray(skel[:rows * k_].reshape(k_, rows).T)
+        return IdResult(idx[:k_].copy(), np.asfortranarray(coeffs[:k_]), sk, k_, res.value, approx)
+
+    def interp_apply(self, dims, strides, coarse, periodic=None, include_boundary=True):
+        d, p, s, nax = _Port._spec(dims, strides, periodic)
+        coarse = _f64(coarse)
+        fine = np.zeros((int(np.prod(dims)), coarse.shape[1]), order="F")
+        self._call(self.lib.ref_interp_apply, d, p, s, nax, int(include_boundary), _dp(coarse),
+                   coarse.shape[1], _dp(fine))
+        return fine
 
     @staticmethod
     def _call(fn, *args):

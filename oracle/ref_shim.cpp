@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "spid/id.hpp"
+#include "spid/interp.hpp"
 #include "spid/metrics.hpp"
 #include "spid/qr.hpp"
 
@@ -213,3 +214,53 @@ int ref_compress_batch(const double* a, std::size_t m, std::size_t n, std::size_
 }
 
 } // extern "C"
+
+namespace {
+spid::SubsampleSpec make_spec(const std::size_t* dims, const int* periodic, const std::size_t* strides,
+                              std::size_t naxes, int include_boundary) {
+    std::vector<std::size_t> d(dims, dims + naxes), s(strides, strides + naxes);
+    std::vector<bool> p(naxes);
+    for (std::size_t i = 0; i < naxes; ++i) p[i] = periodic[i] != 0;
+    return spid::SubsampleSpec::strided(spid::GridGeom::structured(d, p), s, include_boundary != 0);
+}
+}  // namespace
+
+extern "C" {
+
+// spid::spid (proj/src/id.cpp:62-83) + reconstruct(SpidFactors) (id.cpp:92-96).
+int ref_spid(const double* a, std::size_t m, std::size_t n, const std::size_t* dims,
+             const int* periodic, const std::size_t* strides, std::size_t naxes,
+             int include_boundary, int mode, std::size_t k, double tol, std::size_t kcap,
+             std::int64_t* indices, double* coeffs, double* coarse_skel, double* approx,
+             std::size_t* rank, double* resid, char* err, std::size_t errlen) {
+    try {
+        const auto spec = make_spec(dims, periodic, strides, naxes, include_boundary);
+        const spid::SpidFactors f = spid::spid(from_ptr(a, m, n), spec, make_rule(mode, k, tol));
+        if (f.base.achieved_rank > kcap) return fail(spid::Error("InvalidArgument", "kcap"), err, errlen);
+        copy_factors(f.base, kcap, indices, coeffs, coarse_skel, rank, resid);
+        if (approx) {
+            const DenseMatrix r = spid::reconstruct(f);
+            std::memcpy(approx, r.data(), r.entry_count() * sizeof(double));
+        }
+        return 0;
+    } catch (const spid::Error& e) {
+        return fail(e, err, errlen);
+    }
+}
+
+// InterpOperator::from_spec(spec).apply(coarse) (proj/src/interp.cpp:45-100, 168-175).
+int ref_interp_apply(const std::size_t* dims, const int* periodic, const std::size_t* strides,
+                     std::size_t naxes, int include_boundary, const double* coarse, std::size_t k,
+                     double* fine, char* err, std::size_t errlen) {
+    try {
+        const auto spec = make_spec(dims, periodic, strides, naxes, include_boundary);
+        const spid::InterpOperator op = spid::build_interpolator(spec);
+        const DenseMatrix out = op.apply(from_ptr(coarse, op.coarse_cols(), k));
+        std::memcpy(fine, out.data(), out.entry_count() * sizeof(double));
+        return 0;
+    } catch (const spid::Error& e) {
+        return fail(e, err, errlen);
+    }
+}
+
+}  // extern "C"

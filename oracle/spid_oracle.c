@@ -362,3 +362,133 @@ int orc_compression_factor(size_t m, size_t n, size_t stored, double* out) {
     *out = (double)m * (double)n / (double)stored;
     return SPID_OK;
 }
+
+/* ---- strided SubsampleSpec rows + multilinear interpolation -------------- */
+/* Coarse index list of one axis (grid.cpp:91-106). Returns its length. */
+static size_t axis_coarse(size_t dim, size_t stride, int periodic, int incl, size_t* out) {
+    size_t n = 0;
+    for (size_t i = 0; i < dim; i += stride) out[n++] = i;
+    if (incl && !periodic && out[n - 1] != dim - 1) out[n++] = dim - 1;
+    return n;
+}
+
+int orc_row_indices(const size_t* dims, const int* periodic, const size_t* strides, size_t naxes,
+                    int incl, int64_t* rows, size_t cap, size_t* count) {
+    /* grid.cpp:108-130: axis 0 fastest */
+    if (naxes < 1 || naxes > 3) return SPID_BAD_SUBSAMPLE_SPEC;
+    size_t ax[3][4096], na[3] = {1, 1, 1}, d[3] = {1, 1, 1};
+    ax[1][0] = ax[2][0] = 0;
+    for (size_t a = 0; a < naxes; ++a) {
+        if (dims[a] < 2 || dims[a] > 4096 || strides[a] < 1) return SPID_BAD_SUBSAMPLE_SPEC;
+        d[a] = dims[a];
+        na[a] = axis_coarse(dims[a], strides[a], periodic[a], incl, ax[a]);
+    }
+    size_t c = 0;
+    for (size_t i2 = 0; i2 < na[2]; ++i2)
+        for (size_t i1 = 0; i1 < na[1]; ++i1)
+            for (size_t i0 = 0; i0 < na[0]; ++i0) {
+                if (c < cap) rows[c] = (int64_t)(ax[0][i0] + d[0] * ax[1][i1] + d[0] * d[1] * ax[2][i2]);
+                ++c;
+            }
+    *count = c;
+    return SPID_OK;
+}
+
+typedef struct {
+    size_t n, pos[2];
+    double w[2];
+} orc_axisw;
+
+/* interp.cpp:19-41 */
+static int axis_weights(size_t f, const size_t* coarse, size_t nc, size_t dim, int periodic,
+                        orc_axisw* out) {
+    size_t lb = 0;
+    while (lb < nc && coarse[lb] < f) ++lb; /* lower_bound */
+    if (lb < nc && coarse[lb] == f) {
+        out->n = 1;
+        out->pos[0] = lb;
+        out->w[0] = 1.0;
+        return 0;
+    }
+    if (lb == nc) {
+        if (!periodic) return 1; /* ExtrapolationRequired */
+        const size_t last = nc - 1;
+        const double cell = (double)(dim - coarse[last] + coarse[0]);
+        const double w = (double)(f - coarse[last]) / cell;
+        out->n = 2;
+        out->pos[0] = last;
+        out->w[0] = 1.0 - w;
+        out->pos[1] = 0;
+        out->w[1] = w;
+        return 0;
+    }
+    const size_t hi = lb, lo = hi - 1;
+    const double w = (double)(f - coarse[lo]) / (double)(coarse[hi] - coarse[lo]);
+    out->n = 2;
+    out->pos[0] = lo;
+    out->w[0] = 1.0 - w;
+    out->pos[1] = hi;
+    out->w[1] = w;
+    return 0;
+}
+
+/* fine (P x k) = M * coarse (Pc x k): InterpOperator::from_spec (interp.cpp:
+ * 45-100: tensor-product weights, duplicates merged in (a2, a1, a0) order,
+ * columns ascending) applied as apply_column (interp.cpp:177-186). */
+int orc_interp_apply(const size_t* dims, const int* periodic, const size_t* strides, size_t naxes,
+                     int incl, const double* coarse, size_t k, double* fine) {
+    size_t ax[3][4096], na[3] = {1, 1, 1}, d[3] = {1, 1, 1};
+    for (size_t a = 0; a < naxes; ++a) {
+        if (dims[a] < 2 || dims[a] > 4096 || strides[a] < 1) return SPID_BAD_SUBSAMPLE_SPEC;
+        d[a] = dims[a];
+        na[a] = axis_coarse(dims[a], strides[a], periodic[a], incl, ax[a]);
+    }
+    const size_t P = d[0] * d[1] * d[2], Pc = na[0] * na[1] * na[2];
+    const orc_axisw unit = {1, {0, 0}, {1.0, 0.0}};
+    for (size_t i2 = 0; i2 < d[2]; ++i2) {
+        orc_axisw w2 = unit, w1 = unit, w0;
+        if (naxes > 2 && axis_weights(i2, ax[2], na[2], d[2], periodic[2], &w2)) return SPID_GEOMETRY_MISMATCH;
+        for (size_t i1 = 0; i1 < d[1]; ++i1) {
+            if (naxes > 1 && axis_weights(i1, ax[1], na[1], d[1], periodic[1], &w1)) return SPID_GEOMETRY_MISMATCH;
+            for (size_t i0 = 0; i0 < d[0]; ++i0) {
+                if (axis_weights(i0, ax[0], na[0], d[0], periodic[0], &w0)) return SPID_GEOMETRY_MISMATCH;
+                size_t col[8];
+                double wt[8];
+                size_t ne = 0;
+                for (size_t b2 = 0; b2 < w2.n; ++b2)
+                    for (size_t b1 = 0; b1 < w1.n; ++b1)
+                        for (size_t b0 = 0; b0 < w0.n; ++b0) {
+                            size_t c = w0.pos[b0];
+                            if (naxes > 1) c += na[0] * w1.pos[b1];
+                            if (naxes > 2) c += na[0] * na[1] * w2.pos[b2];
+                            const double v = w0.w[b0] * w1.w[b1] * w2.w[b2];
+                            size_t at = ne;
+                            for (size_t q = 0; q < ne; ++q)
+                                if (col[q] == c) at = q;
+                            if (at == ne) {
+                                col[ne] = c;
+                                wt[ne++] = 0.0 + v;
+                            } else {
+                                wt[at] += v;
+                            }
+                        }
+                for (size_t a = 1; a < ne; ++a) /* std::map order: ascending column */
+                    for (size_t b = a; b > 0 && col[b - 1] > col[b]; --b) {
+                        const size_t tc = col[b];
+                        col[b] = col[b - 1];
+                        col[b - 1] = tc;
+                        const double tw = wt[b];
+                        wt[b] = wt[b - 1];
+                        wt[b - 1] = tw;
+                    }
+                const size_t r = i0 + d[0] * (i1 + d[1] * i2);
+                for (size_t t = 0; t < k; ++t) {
+                    double v = 0.0;
+                    for (size_t a = 0; a < ne; ++a) v += wt[a] * coarse[t * Pc + col[a]];
+                    fine[t * P + r] = v;
+                }
+            }
+        }
+    }
+    return SPID_OK;
+}

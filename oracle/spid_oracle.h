@@ -89,6 +89,15 @@ int orc_error_terms(const double* a, size_t m, size_t n, const double* skel, siz
                     const double* coeffs, size_t ldc, size_t rank, double* err2, double* ref2);
 
 int orc_rel_frob_error(const double* exact, const double* approx, size_t count, double* out);
+
+/* SubsampleSpec::row_indices for a strided spec (proj/src/grid.cpp:91-130). */
+int orc_row_indices(const size_t* dims, const int* periodic, const size_t* strides, size_t naxes,
+                    int incl, int64_t* rows, size_t cap, size_t* count);
+
+/* InterpOperator::from_spec(spec).apply(coarse) (proj/src/interp.cpp:19-100,
+ * 168-186): fine (P x k) = M coarse (Pc x k), both column-major. */
+int orc_interp_apply(const size_t* dims, const int* periodic, const size_t* strides, size_t naxes,
+                     int incl, const double* coarse, size_t k, double* fine);
 int orc_compression_factor(size_t m, size_t n, size_t stored, double* out); /* metrics.cpp:5-12 */
 
 #ifdef __cplusplus

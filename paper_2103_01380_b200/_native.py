@@ -49,11 +49,25 @@ class FieldSpec(C.Structure):
                 ("heavy_kmin", C.c_double)]
 
 
+class GridSpec(C.Structure):
+    _fields_ = [("naxes", C.c_int32), ("include_boundary", C.c_int32), ("dims", C.c_int64 * 3),
+                ("strides", C.c_int64 * 3), ("periodic", C.c_int32 * 3), ("nqoi", C.c_int32)]
+
+
+def grid_spec(dims, strides, periodic=None, include_boundary=True, nqoi=1) -> GridSpec:
+    nax = len(dims)
+    per = [int(bool(x)) for x in periodic] if periodic else [0] * nax
+    pad = lambda v, f: list(v) + [f] * (3 - nax)  # noqa: E731
+    return GridSpec(nax, int(bool(include_boundary)), (C.c_int64 * 3)(*pad(dims, 1)),
+                    (C.c_int64 * 3)(*pad(strides, 1)), (C.c_int32 * 3)(*pad(per, 0)), nqoi)
+
+
 _vp = C.c_void_p
 _i64 = C.c_int64
 _H = C.c_void_p
 _RR = C.POINTER(RankRule)
 _OM = C.POINTER(Omega)
+_GS = C.POINTER(GridSpec)
 
 # name -> (restype, argtypes)
 _SIGS = {
@@ -92,6 +106,14 @@ _SIGS = {
                                         _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "spidgpu_field_generate": (C.c_int, [_H, C.POINTER(FieldSpec), _i64, _i64, _vp, _vp, _i64,
                                          _i64, _vp]),
+    "spidgpu_row_indices": (C.c_int, [_GS, _vp, _i64, C.POINTER(C.c_int64)]),
+    "spidgpu_spid": (C.c_int, [_H, _vp, _i64, _i64, _GS, _RR, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "spidgpu_interp_apply": (C.c_int, [_H, _GS, _vp, _i64, _vp]),
+    "spidgpu_spid_reconstruct": (C.c_int, [_H, _GS, _vp, _i64, _vp, _i64, _vp]),
+    "spidgpu_gather_coarse_batched": (C.c_int, [_H, _vp, _i64, _i64, _i64, _i64, _i64, _GS, _vp,
+                                                _i64, _vp, _vp, _i64, _i64, _vp]),
+    "spidgpu_interp_apply_batched": (C.c_int, [_H, _GS, _vp, _i64, _i64, _i64, _vp, _i64, _vp,
+                                               _i64, _i64, _vp]),
 }
 
 

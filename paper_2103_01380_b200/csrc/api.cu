@@ -470,6 +470,69 @@ std::vector<double> make_modes(uint64_t seed, int count, double kmin, double kma
 
 }  // namespace
 
+namespace {
+
+// ---- SPID grid specs ----------------------------------------------------------------
+// Validation of SubsampleSpec::strided / GridGeom::structured (grid.cpp:7-20, 62-75).
+int spec_to_dev(spidgpu_handle h, const spidgpu_grid_spec* sp, GridSpecDev* g, int64_t* P,
+                int64_t* Pc) {
+    if (!sp) return fail(h, SPID_INVALID_ARGUMENT, "null grid spec");
+    if (sp->naxes < 1 || sp->naxes > 3) return fail(h, SPID_BAD_GRID_GEOM, "structured grids have 1 to 3 axes");
+    if (sp->nqoi < 1) return fail(h, SPID_BAD_SUBSAMPLE_SPEC, "nqoi must be >= 1");
+    g->naxes = sp->naxes;
+    g->incl = sp->include_boundary != 0;
+    g->nqoi = sp->nqoi;
+    *P = 1;
+    *Pc = 1;
+    for (int ax = 0; ax < 3; ++ax) {
+        if (ax < sp->naxes) {
+            if (sp->dims[ax] < 2 || sp->dims[ax] > (1 << 20))
+                return fail(h, SPID_BAD_GRID_GEOM, "each structured axis needs at least 2 points");
+            if (sp->strides[ax] < 1) return fail(h, SPID_BAD_SUBSAMPLE_SPEC, "strides must be >= 1");
+            g->dims[ax] = static_cast<int>(sp->dims[ax]);
+            g->strides[ax] = static_cast<int>(sp->strides[ax]);
+            g->periodic[ax] = sp->periodic[ax] != 0;
+            const int64_t base = (sp->dims[ax] + sp->strides[ax] - 1) / sp->strides[ax];
+            const bool extra = g->incl && !g->periodic[ax] && (base - 1) * sp->strides[ax] != sp->dims[ax] - 1;
+            // interp.cpp:25-29: fine points past the last coarse point of a
+            // non-periodic axis cannot be lifted (raised when M is built)
+            if (!g->periodic[ax] && !extra && (base - 1) * sp->strides[ax] != sp->dims[ax] - 1)
+                return fail(h, SPID_EXTRAPOLATION_REQUIRED,
+                            "fine point beyond the last coarse point on a non-periodic axis");
+            *P *= sp->dims[ax];
+            *Pc *= base + (extra ? 1 : 0);
+        } else {
+            g->dims[ax] = 1;
+            g->strides[ax] = 1;
+            g->periodic[ax] = false;
+        }
+    }
+    return SPID_OK;
+}
+
+// SubsampleSpec::row_indices (grid.cpp:108-130), axis 0 fastest, per QoI block.
+std::vector<int64_t> spec_rows(const GridSpecDev& g, int64_t P) {
+    std::vector<int64_t> axes[3];
+    for (int ax = 0; ax < 3; ++ax) {
+        if (ax >= g.naxes) {
+            axes[ax] = {0};
+            continue;
+        }
+        for (int64_t i = 0; i < g.dims[ax]; i += g.strides[ax]) axes[ax].push_back(i);
+        if (g.incl && !g.periodic[ax] && axes[ax].back() != g.dims[ax] - 1)
+            axes[ax].push_back(g.dims[ax] - 1);
+    }
+    std::vector<int64_t> rows;
+    const int64_t d0 = g.dims[0], d1 = g.naxes > 1 ? g.dims[1] : 1;
+    for (int q = 0; q < g.nqoi; ++q)
+        for (int64_t i2 : axes[2])
+            for (int64_t i1 : axes[1])
+                for (int64_t i0 : axes[0]) rows.push_back(q * P + i0 + d0 * i1 + d0 * d1 * i2);
+    return rows;
+}
+
+}  // namespace
+
 // =====================================================================
 extern "C" {
 
@@ -491,6 +554,8 @@ const char* spidgpu_status_name(int status) {
         case SPID_ZERO_DENOMINATOR: return "ZeroDenominator";
         case SPID_BAD_SUBSAMPLE_SPEC: return "BadSubsampleSpec";
         case SPID_EMPTY_SKETCH: return "EmptySketch";
+        case SPID_EXTRAPOLATION_REQUIRED: return "ExtrapolationRequired";
+        case SPID_BAD_GRID_GEOM: return "BadGridGeom";
         case SPID_CUDA_ERROR: return "CudaError";
         case SPID_INVALID_ARGUMENT: return "InvalidArgument";
         case SPID_SHAPE_UNSUPPORTED: return "ShapeUnsupported";
@@ -985,6 +1050,175 @@ int spidgpu_field_generate(spidgpu_handle h, const spidgpu_field_spec* spec, int
     if (dmodes) cudaFree(dmodes);
     if (dheavy) cudaFree(dheavy);
     if (e != cudaSuccess) return cuda_fail(h, e, "launch_field");
+    return SPID_OK;
+}
+
+
+// ---- SPID proper (coarse skeleton + lift) -------------------------------------------
+int spidgpu_row_indices(const spidgpu_grid_spec* spec, int64_t* rows, int64_t cap, int64_t* count) {
+    GridSpecDev g;
+    int64_t P = 0, Pc = 0;
+    const int rc = spec_to_dev(nullptr, spec, &g, &P, &Pc);
+    if (rc) return rc;
+    const std::vector<int64_t> J = spec_rows(g, P);
+    if (count) *count = static_cast<int64_t>(J.size());
+    if (rows)
+        for (int64_t i = 0; i < static_cast<int64_t>(J.size()) && i < cap; ++i) rows[i] = J[i];
+    return SPID_OK;
+}
+
+int spidgpu_spid(spidgpu_handle h, const double* a, int64_t m, int64_t n,
+                 const spidgpu_grid_spec* spec, const spidgpu_rank_rule* rule, int64_t kcap,
+                 int64_t* indices, double* coeffs, double* coarse_skeleton, int64_t* rank,
+                 double* residual_fro) {
+    if (!h) return SPID_INVALID_ARGUMENT;
+    if (m < 1 || n < 1) return fail(h, SPID_EMPTY_MATRIX, "matrix dimensions must be at least 1x1");
+    if (!a) return fail(h, SPID_INVALID_ARGUMENT, "null input");
+    GridSpecDev g;
+    int64_t P = 0, Pc = 0;
+    int rc = spec_to_dev(h, spec, &g, &P, &Pc);
+    if (rc) return rc;
+    if (P * g.nqoi != m)  // id.cpp:70-71
+        return fail(h, SPID_GEOMETRY_MISMATCH, "matrix row count does not match grid point count");
+    const std::vector<int64_t> J = spec_rows(g, P);
+    const int64_t nrows = static_cast<int64_t>(J.size());
+    cudaSetDevice(h->device);
+    Workspace& ws = h->ws[0];
+    cudaStream_t st = h->lanes[0];
+    int64_t lda = 0;
+    rc = matrix_to_dev(h, ws.a, a, m, n, &lda, st);
+    if (rc) return rc;
+    rc = to_dev(h, ws.rows, J.data(), J.size(), st);
+    if (rc) return rc;
+    CK(h, ws.ybuf.ensure(sizeof(double) * nrows * n, st));
+    CK(h, launch_gather_rows(ws.a.as<double>(), m, n, lda, lda * n, 1, ws.rows.as<int64_t>(), nrows,
+                             ws.ybuf.as<double>(), nrows, nrows * n, st));  // subsample, grid.cpp:142-150
+    h->launches += 1;
+    const int64_t kc = std::max<int64_t>(kcap, 1);
+    CK(h, ws.idx.ensure(sizeof(int64_t) * kc, st));
+    CK(h, ws.coeffs.ensure(sizeof(double) * kc * n, st));
+    CK(h, ws.rank.ensure(sizeof(int64_t), st));
+    CK(h, ws.resid.ensure(sizeof(double), st));
+    CK(h, ws.status.ensure(sizeof(int32_t), st));
+    CK(h, cudaMemsetAsync(ws.coeffs.ptr, 0, sizeof(double) * kc * n, st));
+    rc = do_cpqr(h, ws, ws.ybuf.as<double>(), nrows, n, nrows, nrows * n, 1, rule, kc,
+                 ws.idx.as<int64_t>(), ws.coeffs.as<double>(), kc * n, ws.rank.as<int64_t>(),
+                 ws.resid.as<double>(), ws.status.as<int32_t>(), nullptr, nullptr, nullptr, st);
+    if (rc) return rc;
+    // the skeleton stays on the coarse grid: columns I of the sketch B (id.cpp:82)
+    return finish_single(h, ws, nrows, n, kc, ws.ybuf.as<double>(), nrows, indices, coeffs,
+                         coarse_skeleton, rank, residual_fro, st);
+}
+
+int spidgpu_interp_apply(spidgpu_handle h, const spidgpu_grid_spec* spec, const double* coarse,
+                         int64_t k, double* fine) {
+    if (!h) return SPID_INVALID_ARGUMENT;
+    if (!coarse || !fine || k < 1) return fail(h, SPID_INVALID_ARGUMENT, "null buffer / k < 1");
+    GridSpecDev g;
+    int64_t P = 0, Pc = 0;
+    int rc = spec_to_dev(h, spec, &g, &P, &Pc);
+    if (rc) return rc;
+    cudaSetDevice(h->device);
+    Workspace& ws = h->ws[0];
+    cudaStream_t st = h->lanes[0];
+    const int64_t mc = Pc * g.nqoi, m = P * g.nqoi;
+    rc = to_dev(h, ws.skel, coarse, static_cast<size_t>(mc * k), st);
+    if (rc) return rc;
+    CK(h, ws.out.ensure(sizeof(double) * m * k, st));
+    CK(h, ws.flag.ensure(sizeof(int32_t), st));
+    CK(h, cudaMemsetAsync(ws.flag.ptr, 0, sizeof(int32_t), st));
+    CK(h, launch_interp_apply(g, ws.skel.as<double>(), mc, mc * k, k, nullptr, 1,
+                              ws.out.as<double>(), m, m * k, ws.flag.as<int32_t>(), st));
+    h->launches += 1;
+    int32_t flag = 0;
+    CK(h, cudaMemcpyAsync(&flag, ws.flag.ptr, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(h, cudaMemcpyAsync(fine, ws.out.ptr, sizeof(double) * m * k, cudaMemcpyDeviceToHost, st));
+    CK(h, cudaStreamSynchronize(st));
+    if (flag)  // interp.cpp:27-29
+        return fail(h, SPID_GEOMETRY_MISMATCH,
+                    "ExtrapolationRequired: fine point beyond the last coarse point on a non-periodic axis");
+    return SPID_OK;
+}
+
+int spidgpu_spid_reconstruct(spidgpu_handle h, const spidgpu_grid_spec* spec,
+                             const double* coarse_skeleton, int64_t k, const double* coeffs,
+                             int64_t n, double* out) {
+    if (!h) return SPID_INVALID_ARGUMENT;
+    if (!coarse_skeleton || !coeffs || !out || k < 1 || n < 1)
+        return fail(h, SPID_INVALID_ARGUMENT, "bad reconstruct arguments");
+    if (k > 80) return fail(h, SPID_SHAPE_UNSUPPORTED, "reconstruct supports rank <= 80");
+    GridSpecDev g;
+    int64_t P = 0, Pc = 0;
+    int rc = spec_to_dev(h, spec, &g, &P, &Pc);
+    if (rc) return rc;
+    cudaSetDevice(h->device);
+    Workspace& ws = h->ws[0];
+    cudaStream_t st = h->lanes[0];
+    const int64_t mc = Pc * g.nqoi, m = P * g.nqoi;
+    rc = to_dev(h, ws.skel, coarse_skeleton, static_cast<size_t>(mc * k), st);
+    if (rc) return rc;
+    rc = to_dev(h, ws.coeffs, coeffs, static_cast<size_t>(k * n), st);
+    if (rc) return rc;
+    rc = to_dev(h, ws.rank, &k, 1, st);
+    if (rc) return rc;
+    CK(h, ws.a.ensure(sizeof(double) * m * k, st));
+    CK(h, ws.out.ensure(sizeof(double) * m * n, st));
+    CK(h, ws.flag.ensure(sizeof(int32_t), st));
+    CK(h, cudaMemsetAsync(ws.flag.ptr, 0, sizeof(int32_t), st));
+    // id.cpp:95: matmul(interp.apply(skeleton), coeffs)
+    CK(h, launch_interp_apply(g, ws.skel.as<double>(), mc, mc * k, k, nullptr, 1, ws.a.as<double>(),
+                              m, m * k, ws.flag.as<int32_t>(), st));
+    CK(h, launch_reconstruct(ws.a.as<double>(), m, m, m * k, ws.coeffs.as<double>(), k, k * n,
+                             ws.rank.as<int64_t>(), n, 1, ws.out.as<double>(), m, m * n, st));
+    h->launches += 2;
+    int32_t flag = 0;
+    CK(h, cudaMemcpyAsync(&flag, ws.flag.ptr, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(h, cudaMemcpyAsync(out, ws.out.ptr, sizeof(double) * m * n, cudaMemcpyDeviceToHost, st));
+    CK(h, cudaStreamSynchronize(st));
+    if (flag) return fail(h, SPID_GEOMETRY_MISMATCH, "ExtrapolationRequired");
+    return SPID_OK;
+}
+
+int spidgpu_gather_coarse_batched(spidgpu_handle h, const double* A, int64_t m, int64_t n,
+                                  int64_t lda, int64_t strideA, int64_t batch,
+                                  const spidgpu_grid_spec* spec, const int64_t* indices,
+                                  int64_t kcap, const int64_t* rank, double* skel_c,
+                                  int64_t ldskel, int64_t strideS, void* stream) {
+    if (!h) return SPID_INVALID_ARGUMENT;
+    if (!A || !indices || !rank || !skel_c) return fail(h, SPID_INVALID_ARGUMENT, "null pointer");
+    GridSpecDev g;
+    int64_t P = 0, Pc = 0;
+    int rc = spec_to_dev(h, spec, &g, &P, &Pc);
+    if (rc) return rc;
+    if (P * g.nqoi != m) return fail(h, SPID_GEOMETRY_MISMATCH, "m != grid points x nqoi");
+    const std::vector<int64_t> J = spec_rows(g, P);
+    if (ldskel < static_cast<int64_t>(J.size()))
+        return fail(h, SPID_INVALID_ARGUMENT, "ldskel < coarse rows");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Workspace& ws = h->ws[0];
+    rc = to_dev(h, ws.rows, J.data(), J.size(), st);
+    if (rc) return rc;
+    CK(h, launch_gather_coarse(A, lda, strideA, ws.rows.as<int64_t>(), static_cast<int64_t>(J.size()),
+                               indices, kcap, rank, batch, skel_c, ldskel, strideS, st));
+    h->launches += 1;
+    (void)n;
+    return SPID_OK;
+}
+
+int spidgpu_interp_apply_batched(spidgpu_handle h, const spidgpu_grid_spec* spec,
+                                 const double* coarse, int64_t ldc, int64_t strideC, int64_t k,
+                                 const int64_t* rank, int64_t batch, double* fine, int64_t ldf,
+                                 int64_t strideF, void* stream) {
+    if (!h) return SPID_INVALID_ARGUMENT;
+    if (!coarse || !fine) return fail(h, SPID_INVALID_ARGUMENT, "null pointer");
+    GridSpecDev g;
+    int64_t P = 0, Pc = 0;
+    int rc = spec_to_dev(h, spec, &g, &P, &Pc);
+    if (rc) return rc;
+    if (ldc < Pc * g.nqoi || ldf < P * g.nqoi) return fail(h, SPID_INVALID_ARGUMENT, "leading dims");
+    CK(h, launch_interp_apply(g, coarse, ldc, strideC, k, rank, batch, fine, ldf, strideF, nullptr,
+                              static_cast<cudaStream_t>(stream)));
+    h->launches += 1;
     return SPID_OK;
 }
 

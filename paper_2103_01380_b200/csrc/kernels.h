@@ -120,6 +120,24 @@ cudaError_t launch_reconstruct(const double* skel, int64_t m, int64_t ldskel, in
 cudaError_t launch_sqdiff(const double* a, const double* b, int64_t count, double* part,
                           int64_t nparts, cudaStream_t stream);
 
+// ---- SPID coarse skeleton + multilinear lift (interp.cu) -------------------
+struct GridSpecDev {
+    int naxes;
+    int dims[3];
+    int strides[3];
+    bool periodic[3];
+    bool incl;  // SubsampleSpec::include_boundary
+    int nqoi;   // QoI blocks stacked along the rows
+};
+cudaError_t launch_interp_apply(const GridSpecDev& g, const double* coarse, int64_t ldc,
+                                int64_t strideC, int64_t k, const int64_t* rank, int64_t batch,
+                                double* fine, int64_t ldf, int64_t strideF, int32_t* err_flag,
+                                cudaStream_t stream);
+cudaError_t launch_gather_coarse(const double* A, int64_t lda, int64_t strideA, const int64_t* rows,
+                                 int64_t nrows, const int64_t* idx, int64_t kcap,
+                                 const int64_t* rank, int64_t batch, double* skel, int64_t ldskel,
+                                 int64_t strideS, cudaStream_t stream);
+
 // ---- synthetic fields (fields.cu) ----------------------------------------
 struct FieldParams {
     int kind;

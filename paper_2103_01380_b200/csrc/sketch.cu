@@ -229,14 +229,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // Fixed-order reduction of the per-CTA partials of one (subdomain, column
 // tile) into Y (column-major ell x n). Contributors are the CTAs whose chunk
-// range intersects the tile, summed in CTA order.
-__global__ void sketch_reduce_kernel(SketchParams p, int ell_pad, int nt, int64_t nchunk,
+// range intersects the tile, summed in CTA order. One block per (tile, 8-row
+// slab): partial rows are read coalesced (column fastest) into a padded
+// shared slab, then written out column-major (row fastest).
+constexpr int kRedRows = 8;
+constexpr int kRedMaxNt = 256;
+
+__global__ void __launch_bounds__(256) sketch_reduce_kernel(SketchParams p, int ell_pad, int nt, int64_t nchunk,
                                      int64_t ntiles_col, int64_t total_chunks, int G,
                                      int max_segs) {
-    const int64_t tile = blockIdx.x;
+    __shared__ double slab[kRedRows][kRedMaxNt + 1];
+    __shared__ int cfirst, clast;
+    const int nslab = (static_cast<int>(p.ell) + kRedRows - 1) / kRedRows;
+    const int64_t tile = blockIdx.x / nslab;
+    const int r0 = (blockIdx.x % nslab) * kRedRows;
     const int64_t s = tile / ntiles_col, ct = tile % ntiles_col;
     const int64_t t0 = tile * nchunk, t1 = t0 + nchunk;
-    __shared__ int cfirst, clast;
     if (threadIdx.x == 0) {
         int64_t cf = (t0 * G) / total_chunks;
         while (cf > 0 && (cf * total_chunks) / G > t0) --cf;
@@ -247,12 +255,10 @@ __global__ void sketch_reduce_kernel(SketchParams p, int ell_pad, int nt, int64_
         clast = static_cast<int>(cl);
     }
     __syncthreads();
-    const int64_t ncols = p.n - ct * nt < nt ? p.n - ct * nt : nt;
-    const int64_t elems = p.ell * ncols;
-    double* Y = p.Y + s * p.strideY + p.row0;
-    for (int64_t e = threadIdx.x; e < elems; e += blockDim.x) {
-        const int r = static_cast<int>(e % p.ell);
-        const int col = static_cast<int>(e / p.ell);
+    const int ncols = static_cast<int>(p.n - ct * nt < nt ? p.n - ct * nt : nt);
+    const int nrows = static_cast<int>(p.ell - r0 < kRedRows ? p.ell - r0 : kRedRows);
+    for (int e = threadIdx.x; e < nrows * ncols; e += blockDim.x) {
+        const int rl = e / ncols, col = e % ncols;  // column fastest: coalesced partial reads
         double sum = 0.0;
         for (int cc = cfirst; cc <= clast; ++cc) {
             const int64_t lo = (static_cast<int64_t>(cc) * total_chunks) / G;
@@ -261,9 +267,15 @@ __global__ void sketch_reduce_kernel(SketchParams p, int ell_pad, int nt, int64_
             const int segi = static_cast<int>(tile - lo / nchunk);
             const double* part = p.partial + (static_cast<size_t>(cc) * max_segs + segi) *
                                                  (static_cast<size_t>(ell_pad) * nt);
-            sum += part[r * nt + col];
+            sum += part[(r0 + rl) * nt + col];
         }
-        Y[(ct * nt + col) * p.ldy + r] = sum;
+        slab[rl][col] = sum;
+    }
+    __syncthreads();
+    double* Y = p.Y + s * p.strideY + p.row0 + r0;
+    for (int e = threadIdx.x; e < nrows * ncols; e += blockDim.x) {
+        const int rl = e % nrows, col = e / nrows;  // row fastest: contiguous Y column pieces
+        Y[(ct * nt + col) * p.ldy + rl] = slab[rl][col];
     }
 }
 
@@ -294,7 +306,9 @@ cudaError_t launch_t(const SketchParams& p, const SketchPlan& plan, const CUtens
                                                       plan.total_chunks, plan.max_segs);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    sketch_reduce_kernel<<<static_cast<unsigned>(p.batch * plan.ntiles_col), 256, 0, stream>>>(
+    static_assert(Cfg::kNt <= kRedMaxNt, "reduce slab too narrow");
+    const int nslab = static_cast<int>((p.ell + kRedRows - 1) / kRedRows);
+    sketch_reduce_kernel<<<static_cast<unsigned>(p.batch * plan.ntiles_col * nslab), 256, 0, stream>>>(
         p, Cfg::kEllPad, Cfg::kNt, plan.nchunk, plan.ntiles_col, plan.total_chunks, plan.grid,
         plan.max_segs);
     return cudaGetLastError();

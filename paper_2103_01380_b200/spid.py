@@ -19,7 +19,7 @@ from ._native import SpidError
 __all__ = [
     "SpidError", "RankRule", "column_id", "column_id_at_most", "qr", "sub_id", "sketch_id",
     "reconstruct", "rel_frob_error", "compression_factor", "philox_omega", "row_indices",
-    "make_block_domains", "IdFactors",
+    "make_block_domains", "IdFactors", "SpidFactors", "spid", "interp_apply", "spid_reconstruct",
 ]
 
 
@@ -277,6 +277,79 @@ def sketch_id(a, ell, rank=None, tol=None, *, omega=None, seed=0, subdomain=0, r
     k = rk.value
     return IdFactors(idx[:k].copy(), np.asfortranarray(coeffs[:k]), np.asfortranarray(skel[:, :k]),
                      n, k, res.value, y)
+
+
+@dataclass
+class SpidFactors:
+    """spid::SpidFactors (proj/include/spid/id.hpp:21-24): base factors with the
+    skeleton on the coarse rows J, plus the (recipe-stored) lift spec."""
+    base: IdFactors
+    spec: object  # _native.GridSpec
+
+    def stored_entries(self) -> int:
+        """k (m_c + n): the coarse skeleton plus the coefficients
+        (proj/src/metrics.hpp:13-16, archive.cpp:180-184)."""
+        return self.base.skeleton.size + self.base.coeffs.size
+
+
+def spid(a, dims, strides, rank=None, tol=None, periodic=None, *, include_boundary=True,
+         rule=None, reconstruct_approx=True, device=0):
+    """spid::spid (proj/src/id.cpp:62-83) / pyspid.spid: row-subsample sketch
+    B = A(J, :), column ID of B, skeleton kept on the coarse grid; returns
+    pyspid's dict (indices, coeffs, skeleton (coarse), rank, approx) plus the
+    SpidFactors under "factors"."""
+    a = _f64(a)
+    m, n = a.shape
+    spec = N.grid_spec(dims, strides, periodic, include_boundary)
+    cnt = C.c_int64(0)
+    rc = N.lib.spidgpu_row_indices(C.byref(spec), None, 0, C.byref(cnt))
+    if rc:
+        raise SpidError(N.status_name(rc), "bad subsample spec")
+    mc = cnt.value
+    r = _rule(rank, tol, rule)
+    kcap = r.cap(mc, n)
+    idx = np.zeros(kcap, dtype=np.int64)
+    coeffs = np.zeros((kcap, n), order="F")
+    skel = np.zeros((mc, kcap), order="F")
+    rk, res = C.c_int64(0), C.c_double(0)
+    h = _h(device)
+    h.check(N.lib.spidgpu_spid(h.h, _ptr(a), m, n, C.byref(spec), C.byref(r.c()), kcap, _ptr(idx),
+                               _ptr(coeffs), _ptr(skel), C.byref(rk), C.byref(res)))
+    k = rk.value
+    f = IdFactors(idx[:k].copy(), np.asfortranarray(coeffs[:k]), np.asfortranarray(skel[:, :k]),
+                  n, k, res.value)
+    out = f.as_dict()
+    out["factors"] = SpidFactors(f, spec)
+    if reconstruct_approx:
+        out["approx"] = spid_reconstruct(out["factors"], device=device)
+    return out
+
+
+def interp_apply(dims, strides, coarse, periodic=None, *, include_boundary=True, nqoi=1, device=0):
+    """InterpOperator::from_spec(spec).apply(coarse) (proj/src/interp.cpp:
+    45-100, 168-186) on the GPU: the multilinear lift of coarse columns."""
+    c = _f64(coarse)
+    spec = N.grid_spec(dims, strides, periodic, include_boundary, nqoi)
+    P = int(np.prod(dims)) * nqoi
+    fine = np.zeros((P, c.shape[1]), order="F")
+    h = _h(device)
+    h.check(N.lib.spidgpu_interp_apply(h.h, C.byref(spec), _ptr(c), c.shape[1], _ptr(fine)))
+    return fine
+
+
+def spid_reconstruct(factors: SpidFactors, *, device=0):
+    """spid::reconstruct(SpidFactors) (proj/src/id.cpp:92-96): M * skel_c * C."""
+    f = factors.base
+    s, c = _f64(f.skeleton), _f64(f.coeffs)
+    m = 1
+    for ax in range(factors.spec.naxes):
+        m *= int(factors.spec.dims[ax])
+    m *= int(factors.spec.nqoi)
+    out = np.zeros((m, c.shape[1]), order="F")
+    h = _h(device)
+    h.check(N.lib.spidgpu_spid_reconstruct(h.h, C.byref(factors.spec), _ptr(s), s.shape[1],
+                                           _ptr(c), c.shape[1], _ptr(out)))
+    return out
 
 
 def reconstruct(skeleton, coeffs=None, *, device=0):
