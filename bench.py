@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-quality", action="store_true")
     return ap.parse_args()
 
 
@@ -71,6 +72,20 @@ def workload(cfg_name, rank, world):
         lo, hi = contiguous_range(cfg.subdomains, rank, world)
         field, first, count = cfg, lo, hi - lo
     return cfg, field, first, count
+
+
+def _allreduce(t, op=None):
+    """All-reduce on the job's backend: NCCL in place on the device tensor; the
+    gloo functional-check mode (BENCH_BACKEND=gloo) goes through the host."""
+    import torch.distributed as dist
+
+    op = dist.ReduceOp.SUM if op is None else op
+    if dist.get_backend() == "nccl":
+        dist.all_reduce(t, op=op)
+    else:
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        t.copy_(h)
 
 
 def load_json(path):
@@ -219,9 +234,16 @@ def run_ours(args):
     from paper_2103_01380_b200.engine import Engine, rule_for
 
     rank, world, local = dist_env()
+    # one process per GPU; local % count only matters for the 1-GPU functional
+    # check of the multi-rank path (BENCH_BACKEND=gloo), never for numbers
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     cfg, field, first, count = workload(args.config, rank, world)
     eng = Engine(local)
     dev = eng.dev
@@ -248,7 +270,7 @@ def run_ours(args):
         eng.h.check(_gather_into(eng, A, res))
         sums = torch.stack([res.residual_fro.square().sum(), res.rank.sum().double()])
         if world > 1:
-            dist.all_reduce(sums)
+            _allreduce(sums)
         return sums
 
     for _ in range(args.warmup):
@@ -273,7 +295,7 @@ def run_ours(args):
     sk_ms = sum(a.elapsed_time(b) for a, b in ev_sk) / len(ev_sk)
     tm = torch.tensor([ms, sk_ms], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        _allreduce(tm, op=dist.ReduceOp.MAX)
     ms, sk_ms = float(tm[0]), float(tm[1])
     ms_step = ms / args.steps
     raw_local = cfg.raw_bytes(count)
@@ -296,7 +318,7 @@ def run_ours(args):
     report = D.reduce_report(sums)
     vt = torch.tensor([verify_ms], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(vt, op=dist.ReduceOp.MAX)
+        _allreduce(vt, op=dist.ReduceOp.MAX)
     verify_ms = float(vt[0])
 
     # roofline of the dominant kernel (the sketch)
@@ -338,6 +360,8 @@ def run_ours(args):
         "roofline": roofline,
     }
 
+    if not args.no_quality:
+        line["quality_spid"] = quality_spid(eng, cfg, field, A, first, count, world, stream)
     if not args.no_e2e:
         line["e2e"] = e2e_measure(eng, cfg, A, first, count, rule, args, world)
     if world > 1:
@@ -385,6 +409,55 @@ def _gather_into(eng, A, res):
                                         C.c_void_p(torch.cuda.current_stream().cuda_stream))
 
 
+def quality_spid(eng, cfg, field, A, first, count, world, stream):
+    """The BASELINE quality target ("CF > 100 at rel. error <= 1e-3") on the
+    same subdomains: SPID proper -- Gaussian-sketch column
+    selection with an adaptive rank (blocked rule, steps of 2 up to 64, sketch
+    error <= 3e-4), skeleton stored on the stride-2 coarse grid and lifted
+    with the reference's multilinear operator. Untimed quality pass, then a
+    timed compress of the same variant (sketch with ell = 80 + CPQR + coarse
+    gather)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2103_01380_b200 import distributed as D
+    from paper_2103_01380_b200.spid import RankRule
+
+    rule = RankRule.blocked(64, 2, 3e-4)
+    ell = 64 + cfg.p
+    spec = eng.block_spec(field, 2)
+    mc = eng.coarse_rows(spec)
+    r = eng.compress(A, ell, rule, seed=cfg.seed, subdomain_base=first, want_skel=False)
+    r.check()
+    sc = eng.gather_coarse(A, r, spec)
+    e2, r2 = eng.verify_coarse(A, r, sc, spec)
+    ks = r.rank.double()
+    sums = torch.stack([e2.sum(), r2.sum(), (ks * (mc + cfg.n)).sum(),
+                        torch.tensor(float(cfg.m) * cfg.n * count, dtype=torch.float64, device=eng.dev)])
+    rep = D.reduce_report(sums)
+    # timed compress of this variant
+    reps = 5
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0.record(stream)
+    for _ in range(reps):
+        eng.compress(A, ell, rule, seed=cfg.seed, subdomain_base=first, want_skel=False, out=r)
+        eng.gather_coarse(A, r, spec)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([t0.elapsed_time(t1) / reps], dtype=torch.float64, device=eng.dev)
+    if world > 1:
+        _allreduce(ms, op=dist.ReduceOp.MAX)
+    return {"variant": "SPID coarse skeleton (stride 2, trilinear lift) + blocked rank (step 2, "
+                       "kmax 64, sketch tol 3e-4), ell = 80",
+            "cf": rep.cf, "rel_frob_error": rep.rel_frob_error, "m_c": mc,
+            "mean_rank": float(ks.mean()), "max_rank": int(ks.max()),
+            "ms_per_step": float(ms[0]),
+            "raw_gbs": cfg.raw_bytes(count) * world / (float(ms[0]) / 1e3) / 1e9}
+
+
 def e2e_measure(eng, cfg, A, first, count, rule, args, world):
     """The same metric through the C-ABI host call (spidgpu_compress_host):
     pinned host A in, host factors out, every copy inside the timed region."""
@@ -414,7 +487,7 @@ def e2e_measure(eng, cfg, A, first, count, rule, args, world):
     el = torch.tensor([(time.perf_counter() - t) / args.e2e_steps], dtype=torch.float64,
                       device=eng.dev)
     if world > 1:
-        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        _allreduce(el, op=dist.ReduceOp.MAX)
     sec = float(el[0])
     h2d = a_host.numel() * 8
     d2h = sum(v.numel() * v.element_size() for v in out.values())

@@ -59,6 +59,8 @@ def reduce_report(sums: torch.Tensor, group=None, block_ranks=None) -> QualityRe
     """All-reduce the 4 sums (if a process group is up) and form the report."""
     v = sums.clone()
     if dist.is_available() and dist.is_initialized():
+        if dist.get_backend(group) != "nccl":
+            v = v.cpu()  # gloo reduces host tensors
         dist.all_reduce(v, op=dist.ReduceOp.SUM, group=group)
     e2, r2, stored, raw = (float(x) for x in v.cpu())
     if r2 == 0.0:

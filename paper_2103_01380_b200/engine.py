@@ -173,6 +173,57 @@ class Engine:
                                                   m * r.kcap, _stream(stream)))
         return skel
 
+    # ---- SPID proper: coarse-grid skeleton + multilinear lift ------
+    @staticmethod
+    def block_spec(cfg: SpidConfig, stride: int) -> N.GridSpec:
+        """The subdomain's local grid: a b^3 block of the periodic N^3 grid is
+        periodic along an axis only if it covers it (proj/src/blocking.cpp:
+        84-92); non-periodic local axes pin their last point (grid.cpp:101)."""
+        per = [cfg.block == cfg.grid] * 3
+        return N.grid_spec([cfg.block] * 3, [stride] * 3, per, True, cfg.qois)
+
+    @staticmethod
+    def coarse_rows(spec: N.GridSpec) -> int:
+        cnt = C.c_int64(0)
+        rc = N.lib.spidgpu_row_indices(C.byref(spec), None, 0, C.byref(cnt))
+        if rc:
+            raise SpidError(N.status_name(rc), "bad grid spec")
+        return cnt.value
+
+    def gather_coarse(self, A: torch.Tensor, r: CompressResult, spec: N.GridSpec,
+                      stream=None) -> torch.Tensor:
+        """skel_c_s = A_s(J, I_s): the SPID skeleton kept on the coarse rows."""
+        S, n, m = A.shape
+        mc = self.coarse_rows(spec)
+        skel = torch.zeros((S, r.kcap, mc), dtype=torch.float64, device=self.dev)
+        self.h.check(N.lib.spidgpu_gather_coarse_batched(
+            self.h.h, _p(A), m, n, m, m * n, S, C.byref(spec), _p(r.indices), r.kcap, _p(r.rank),
+            _p(skel), mc, mc * r.kcap, _stream(stream)))
+        return skel
+
+    def lift(self, skel_c: torch.Tensor, r: CompressResult, spec: N.GridSpec, m: int,
+             stream=None) -> torch.Tensor:
+        """M * skel_c per subdomain (InterpOperator::apply, bit-exact)."""
+        S, kcap, mc = skel_c.shape
+        fine = torch.zeros((S, kcap, m), dtype=torch.float64, device=self.dev)
+        self.h.check(N.lib.spidgpu_interp_apply_batched(
+            self.h.h, C.byref(spec), _p(skel_c), mc, mc * kcap, kcap, _p(r.rank), S, _p(fine), m,
+            m * kcap, _stream(stream)))
+        return fine
+
+    def verify_coarse(self, A: torch.Tensor, r: CompressResult, skel_c: torch.Tensor,
+                      spec: N.GridSpec, stream=None):
+        """(err2, ref2) of the SPID reconstruction M * skel_c * C
+        (spid::reconstruct(SpidFactors), proj/src/id.cpp:92-96)."""
+        S, n, m = A.shape
+        lifted = self.lift(skel_c, r, spec, m, stream)
+        saved = r.skel
+        r.skel = lifted
+        try:
+            return self.verify(A, r, stream)
+        finally:
+            r.skel = saved
+
     def reconstruct(self, r: CompressResult, stream=None) -> torch.Tensor:
         S = r.rank.shape[0]
         out = torch.empty((S, r.n, r.m), dtype=torch.float64, device=self.dev)
