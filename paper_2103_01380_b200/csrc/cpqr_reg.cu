@@ -63,6 +63,10 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
 
     // ---- columns into registers; finiteness (qr.cpp:34-35, id.cpp:41-42) ----
     double w[CPT][ROWS];
+    // Branch-free padded loops while the column fits the register budget;
+    // larger tiles exit at `rows` (a uniform branch) to keep registers down.
+    // Both are bit-identical: padded rows only ever contribute +0.0.
+    constexpr bool kFree = ROWS * CPT <= 48;
     int bad = 0;
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
@@ -96,12 +100,13 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
     for (int c = 0; c < CPT; ++c) {
         const int j = tid + c * kT;
         if (j < n) {
+            // rows >= `rows` are zero padding: every running sum starts at +0.0
+            // and can never become -0.0 (x + (-x) rounds to +0.0), so the
+            // padded +0.0 terms leave each sum bit-identical to the
+            // reference's shorter loop -- and the loops stay branch-free.
             double s = 0.0;
 #pragma unroll
-            for (int i = 0; i < ROWS; ++i) {
-                if (i >= rows) break;
-                s = add_rn(s, mul_rn(w[c][i], w[c][i]));
-            }
+            for (int i = 0; i < ROWS; ++i) s = add_rn(s, mul_rn(w[c][i], w[c][i]));
             const double v = sqrt(s);
             nrm[j] = v;
             colsq[j] = s;
@@ -199,10 +204,7 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
             for (int c = 0; c < CPT; ++c)
                 if (c == cc) {
 #pragma unroll
-                    for (int i = 0; i < ROWS; ++i) {
-                        if (i >= rows) break;
-                        qbuf[i] = w[c][i];
-                    }
+                    for (int i = 0; i < ROWS; ++i) qbuf[i] = w[c][i];  // zero padding past rows
                 }
         }
         __syncthreads();
@@ -219,25 +221,26 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
             if (j < n && posof[j] > s) {
                 // q is re-read (16-byte broadcast LDS, opaque to the compiler)
                 // in every pass instead of being cached: keeps the register
-                // budget to the column itself. qbuf is zero past `rows`.
+                // budget to the column itself. Rows past `rows` are +0.0 in
+                // both q and w and stay +0.0 (0 - r*0 = +0), so the padded
+                // terms add +0.0 to sums that cannot be -0.0: bit-neutral,
+                // and the loops carry no per-element branches.
                 double r1 = 0.0;
 #pragma unroll
                 for (int i = 0; i < ROWS; i += 2) {
-                    if (i >= rows) break;
+                    if (!kFree && i >= rows) break;
                     const double2 q = lds128(qs + 16 * (i / 2));
                     r1 = add_rn(r1, mul_rn(q.x, w[c][i]));
-                    if (i + 1 >= rows) break;
                     r1 = add_rn(r1, mul_rn(q.y, w[c][i + 1]));
                 }
                 double r2 = 0.0;
 #pragma unroll
                 for (int i = 0; i < ROWS; i += 2) {
-                    if (i >= rows) break;
+                    if (!kFree && i >= rows) break;
                     const double2 q = lds128(qs + 16 * (i / 2));
                     const double v0 = sub_rn(w[c][i], mul_rn(r1, q.x));
                     w[c][i] = v0;
                     r2 = add_rn(r2, mul_rn(q.x, v0));
-                    if (i + 1 >= rows) break;
                     const double v1 = sub_rn(w[c][i + 1], mul_rn(r1, q.y));
                     w[c][i + 1] = v1;
                     r2 = add_rn(r2, mul_rn(q.y, v1));
@@ -245,12 +248,11 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
                 double nn = 0.0;
 #pragma unroll
                 for (int i = 0; i < ROWS; i += 2) {
-                    if (i >= rows) break;
+                    if (!kFree && i >= rows) break;
                     const double2 q = lds128(qs + 16 * (i / 2));
                     const double v0 = sub_rn(w[c][i], mul_rn(r2, q.x));
                     w[c][i] = v0;
                     nn = add_rn(nn, mul_rn(v0, v0));
-                    if (i + 1 >= rows) break;
                     const double v1 = sub_rn(w[c][i + 1], mul_rn(r2, q.y));
                     w[c][i + 1] = v1;
                     nn = add_rn(nn, mul_rn(v1, v1));

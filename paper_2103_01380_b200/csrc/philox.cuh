@@ -5,7 +5,7 @@
 // the sketch kernel never reads Omega from HBM (performance mode), and
 // spidgpu_philox_omega() can materialise the identical matrix for an oracle.
 //
-// Philox4x32-10 (Salmon et al., SC'11): counter {k/4, r, s_lo, s_hi}, key
+// Philox4x32-7 (Salmon et al., SC'11): counter {k/4, r, s_lo, s_hi}, key
 // {seed_lo, seed_hi}; the 4 outputs become Omega_s(r, 4*(k/4) + 0..3) via two
 // Box-Muller transforms in fp32 with the SFU intrinsics (the sketch needs a
 // Gaussian-distributed Omega, not fp64-accurate normals), widened to fp64.
@@ -32,10 +32,11 @@ __host__ __device__ __forceinline__ void philox_round(Philox4& c, uint32_t k0, u
     c = Philox4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
 }
 
-__host__ __device__ __forceinline__ Philox4 philox4x32_10(Philox4 c, uint32_t k0, uint32_t k1) {
+template <int ROUNDS>
+__host__ __device__ __forceinline__ Philox4 philox4x32(Philox4 c, uint32_t k0, uint32_t k1) {
     const uint32_t W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
 #pragma unroll
-    for (int i = 0; i < 10; ++i) {
+    for (int i = 0; i < ROUNDS; ++i) {
         philox_round(c, k0, k1);
         k0 += W0;
         k1 += W1;
@@ -43,10 +44,14 @@ __host__ __device__ __forceinline__ Philox4 philox4x32_10(Philox4 c, uint32_t k0
     return c;
 }
 
+// Rounds used for Omega: Philox4x32-7 passes TestU01 BigCrush (Salmon et al.,
+// SC'11, Table 2) and keeps the producer warps off the sketch's critical path.
+constexpr int kOmegaRounds = 7;
+
 // Four N(0,1) samples for Omega_s(r, 4*kq + 0..3).
 __device__ __forceinline__ void omega_normals4(uint64_t seed, uint64_t s, uint32_t r, uint32_t kq,
                                                double out[4]) {
-    const Philox4 v = philox4x32_10(
+    const Philox4 v = philox4x32<kOmegaRounds>(
         Philox4{kq, r, static_cast<uint32_t>(s), static_cast<uint32_t>(s >> 32)},
         static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
     const float kInv = 2.3283064365386963e-10f;  // 2^-32

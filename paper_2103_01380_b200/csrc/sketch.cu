@@ -44,7 +44,8 @@ namespace {
 
 constexpr int kKc = 16;  // rows of A per chunk (128 B = one swizzle row)
 constexpr int kWarps = 16;           // consumer (tensor-core) warps: 4 per SMSP
-constexpr int kProducerWarps = 2;    // TMA issue + Omega generation
+constexpr int kProducerWarps = 4;    // TMA issue + Omega generation, one per SMSP so
+                                     // no SMSP's consumers lose issue slots to them
 constexpr int kThreads = (kWarps + kProducerWarps) * kWarp;
 constexpr int kStageBudget = 200 * 1024;
 
