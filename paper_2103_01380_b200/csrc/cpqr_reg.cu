@@ -136,13 +136,16 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
     // ---- greedy pivoting loop (qr.cpp:61-106) ---------------------------------
     int rank = 0;
     const int step_limit = static_cast<int>(p.step_limit);
+    bool alive[CPT];  // column not yet selected (position >= s), kept in registers
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) alive[c] = tid + c * kT < n;
     for (int s = 0; s < step_limit; ++s) {
         double bv = -1.0;
         int bi = 0x7fffffff;
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
             const int j = tid + c * kT;
-            if (j < n && posof[j] >= s && key_better(nrm[j], j, bv, bi)) {
+            if (alive[c] && key_better(nrm[j], j, bv, bi)) {
                 bv = nrm[j];
                 bi = j;
             }
@@ -153,49 +156,52 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
             red_i[warp] = bi;
         }
         __syncthreads();
-        if (tid == 0) {
-            double v = red_v[0];
-            int ix = red_i[0];
-            for (int k = 1; k < kT / kWarp; ++k)
-                if (key_better(red_v[k], red_i[k], v, ix)) {
-                    v = red_v[k];
-                    ix = red_i[k];
-                }
-            int stop = 0;
-            if (p.mode == RULE_TOL && v <= p.tol * max_init) stop = 1;  // qr.cpp:74-76
-            if (!stop && p.mode == RULE_BLOCKED && s > 0 && s % p.kstep == 0) {
+        // every thread reduces the 8 warp partials in the same order (a total
+        // order, so the same winner); no serial section, no broadcast barrier
+        double v = red_v[0];
+        int ix = red_i[0];
+#pragma unroll
+        for (int k = 1; k < kT / kWarp; ++k)
+            if (key_better(red_v[k], red_i[k], v, ix)) {
+                v = red_v[k];
+                ix = red_i[k];
+            }
+        int stop = 0;
+        if (p.mode == RULE_TOL && v <= p.tol * max_init) stop = 1;  // qr.cpp:74-76
+        if (p.mode == RULE_BLOCKED && s > 0 && s % p.kstep == 0) {
+            // residual_fro after s steps in position order (qr.cpp:111-115):
+            // a serial sum, computed by one thread and broadcast
+            if (tid == 0) {
                 double rsq = 0.0;
                 for (int pos = s; pos < n; ++pos) {
                     const double nj = nrm[perm[pos]];
                     rsq = add_rn(rsq, mul_rn(nj, nj));
                 }
-                if (sqrt(rsq) <= p.tol * sh.yfro) stop = 1;
+                sh.flag = sqrt(rsq) <= p.tol * sh.yfro;
             }
-            if (!stop && v < kCollapseRel * max_init)  // qr.cpp:77-81
-                stop = (p.mode == RULE_FIXED && p.strict) ? 2 : 1;
-            if (!stop) {  // qr.cpp:83-87
-                const int ps = posof[ix], cs = perm[s];
-                perm[s] = ix;
-                perm[ps] = cs;
-                posof[ix] = s;
-                posof[cs] = ps;
-                R[static_cast<size_t>(s) * n + ix] = v;  // qr.cpp:89-90
-                diag[s] = v;
-            }
-            sh.best_v = v;
-            sh.best_i = ix;
-            sh.stop = stop;
+            __syncthreads();
+            if (sh.flag) stop = 1;
         }
-        __syncthreads();
-        if (sh.stop) {
-            if (sh.stop == 2) {
+        if (!stop && v < kCollapseRel * max_init)  // qr.cpp:77-81
+            stop = (p.mode == RULE_FIXED && p.strict) ? 2 : 1;
+        if (stop) {
+            if (stop == 2) {
                 finish_error(SPID_RANK_UNREACHABLE);
                 return;
             }
             break;
         }
-        const int pc = sh.best_i;
-        const double pn = sh.best_v;
+        if (tid == 0) {  // position bookkeeping (qr.cpp:83-87), read only after the loop
+            const int ps = posof[ix], cs = perm[s];
+            perm[s] = ix;
+            perm[ps] = cs;
+            posof[ix] = s;
+            posof[cs] = ps;
+            R[static_cast<size_t>(s) * n + ix] = v;  // qr.cpp:89-90
+            diag[s] = v;
+        }
+        const int pc = ix;
+        const double pn = v;
         // the owner publishes its column; `rows` threads normalise it in
         // parallel, q_s = w_s / R(s,s) (qr.cpp:91-92)
         if ((pc % kT) == tid) {
@@ -203,6 +209,7 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
 #pragma unroll
             for (int c = 0; c < CPT; ++c)
                 if (c == cc) {
+                    alive[c] = false;
 #pragma unroll
                     for (int i = 0; i < ROWS; ++i) qbuf[i] = w[c][i];  // zero padding past rows
                 }
@@ -218,7 +225,7 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
             const int j = tid + c * kT;
-            if (j < n && posof[j] > s) {
+            if (alive[c]) {
                 // q is re-read (16-byte broadcast LDS, opaque to the compiler)
                 // in every pass instead of being cached: keeps the register
                 // budget to the column itself. Rows past `rows` are +0.0 in
