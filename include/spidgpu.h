@@ -273,6 +273,64 @@ int spidgpu_compress_host(spidgpu_handle h, const double* a, int64_t m, int64_t 
                           double* err2, double* ref2);
 
 /* =====================================================================
+ * Archive codec (proj/include/spid/archive.hpp) -- SURVEY 8(f)3.
+ * ===================================================================== */
+
+/* CRC-32/ISO-HDLC of a buffer (spid::crc32, proj/src/archive.cpp:168-178),
+ * computed on the device. on_device != 0: `data` is a device pointer. */
+int spidgpu_crc32(spidgpu_handle h, const void* data, int64_t nbytes, int32_t on_device,
+                  uint32_t* out);
+
+#define SPIDGPU_ARCHIVE_EXACT 0  /* column ID of each block's coarse rows: the
+                                    reference's spid() -> byte-identical archive */
+#define SPIDGPU_ARCHIVE_SKETCH 1 /* Gaussian sketch (Philox) of the coarse rows
+                                    first, then the column ID (FP64 tensor cores) */
+typedef struct spidgpu_archive_spec {
+    int32_t naxes;              /* structured grid, 1..3 axes (axis 0 fastest)  */
+    int32_t mode;               /* SPIDGPU_ARCHIVE_*                            */
+    int64_t dims[3];
+    int32_t periodic[3];
+    int32_t reserved;
+    int64_t blocks_per_axis[3]; /* make_block_domains plan                      */
+    int64_t strides[3];         /* SubsampleSpec::strided(local, strides, true) */
+    int64_t ell;                /* SKETCH: sketch rows (>= rank)                 */
+    uint64_t seed;              /* SKETCH: Philox key; block b uses subdomain b  */
+    const char* qoi;            /* metadata strings (may be NULL = "")          */
+    const char* provenance;
+} spidgpu_archive_spec;
+
+/* Batch compression of a whole field into an archive -- the spid CLI's
+ * `compress --chunk 0` on a structured grid (compress_structured_batch,
+ * proj/tools/spid_cli.cpp:195-232) followed by spid::encode
+ * (proj/src/archive.cpp:193-212). a: m x n (ld lda), rows = grid points
+ * (axis 0 fastest); a_on_device != 0 if `a` is a device pointer. rule: FIXED
+ * (at_most = 0) or TOL, as the CLI's --rank / --tol. The archive is kept in
+ * the handle: *nbytes receives its size, spidgpu_archive_fetch copies it. */
+int spidgpu_archive_compress(spidgpu_handle h, const double* a, int64_t m, int64_t n, int64_t lda,
+                             int32_t a_on_device, const spidgpu_archive_spec* spec,
+                             const spidgpu_rank_rule* rule, int64_t* nbytes);
+int spidgpu_archive_fetch(spidgpu_handle h, uint8_t* dst, int64_t cap);
+
+/* decode() header walk (archive.cpp:214-249) without the checksums: output
+ * shape of decompress (rows = grid points, cols = snapshot count) and the
+ * block count. Host-only. */
+int spidgpu_archive_shape(const uint8_t* bytes, int64_t nbytes, int64_t* rows, int64_t* cols,
+                          int64_t* blocks);
+
+/* archive_info_json (archive.cpp:260-268) of an archive (checksums verified
+ * on the device). Writes a NUL-terminated string; *len = strlen. */
+int spidgpu_archive_info(spidgpu_handle h, const uint8_t* bytes, int64_t nbytes, char* out,
+                         int64_t cap, int64_t* len);
+
+/* decode() + decompress() (archive.cpp:214-249, 281-303): every section
+ * checksummed on the device, coarse skeletons lifted, blocks multiplied out
+ * in the reference matmul's order and scattered into out (rows x cols, ld
+ * ldo; out_on_device != 0 for a device pointer). Bit-identical to the
+ * reference's decompress. */
+int spidgpu_archive_decompress(spidgpu_handle h, const uint8_t* bytes, int64_t nbytes, double* out,
+                               int64_t ldo, int32_t out_on_device);
+
+/* =====================================================================
  * Synthetic input fields (bench/tests only; not a reference interface).
  * Taylor-Green-vortex families of BASELINE.json configs 1-5, generated in
  * place on the device for a batch of subdomains of a periodic N^3 grid split

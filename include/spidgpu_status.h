@@ -30,6 +30,14 @@ enum spidgpu_status {
     SPID_EMPTY_SKETCH = 15,     /* "EmptySketch"      grid.cpp:78,110 */
     SPID_EXTRAPOLATION_REQUIRED = 16, /* "ExtrapolationRequired" interp.cpp:27-29 */
     SPID_BAD_GRID_GEOM = 17,    /* "BadGridGeom"      grid.cpp:8-14 */
+    SPID_BLOCK_TOO_SMALL = 18,  /* "BlockTooSmall"    blocking.cpp:14-15,21 */
+    SPID_BAD_MAGIC = 19,        /* "BadMagic"         archive.cpp:219 */
+    SPID_VERSION_UNSUPPORTED = 20,/* "VersionUnsupported" archive.cpp:222 */
+    SPID_TRUNCATED_PAYLOAD = 21,/* "TruncatedPayload" archive.cpp:71,112,229,242,247 */
+    SPID_CHECKSUM_MISMATCH = 22,/* "ChecksumMismatch" archive.cpp:92 */
+    SPID_COVERAGE_GAP = 23,     /* "CoverageGap"      archive.cpp:285; blocking.cpp:236 */
+    SPID_UNSTRUCTURED_NO_INTERP = 24,/* "UnstructuredNoInterp" archive.cpp:291; interp.cpp:47 */
+    SPID_BAD_STREAM_CONFIG = 25,/* "BadStreamConfig"  spid_cli.cpp:248-263 */
     /* codes that exist only on the device path */
     SPID_CUDA_ERROR = 100,      /* "CudaError" */
     SPID_INVALID_ARGUMENT = 101,/* "InvalidArgument" (null pointer, bad leading dim) */

@@ -35,6 +35,8 @@ STATUS_NAMES = {
     7: "BadRankRule", 8: "EmptyMatrix", 9: "EmptySelection",
     10: "IndexOutOfRange", 11: "GeometryMismatch", 12: "ZeroReference",
     13: "ZeroDenominator", 14: "BadSubsampleSpec", 15: "EmptySketch", 16: "ExtrapolationRequired", 17: "BadGridGeom",
+    18: "BlockTooSmall", 19: "BadMagic", 20: "VersionUnsupported", 21: "TruncatedPayload",
+    22: "ChecksumMismatch", 23: "CoverageGap", 24: "UnstructuredNoInterp", 25: "BadStreamConfig",
     100: "CudaError", 101: "InvalidArgument", 102: "ShapeUnsupported", 103: "NoDevice",
 }
 
@@ -305,7 +307,50 @@ class _Ref:
                                _sz, C.c_double, _sz, _I64, _D, _D, _D, _SZ, _D, cp, _sz]
         L.ref_interp_apply.argtypes = [_SZ, C.POINTER(C.c_int), _SZ, _sz, C.c_int, _D, _sz, _D,
                                        cp, _sz]
+        L.ref_compress_field.argtypes = [_D, _sz, _sz, _SZ, C.POINTER(C.c_int), _sz, _SZ, _SZ, _sz,
+                                         C.c_double, cp, cp, _SZ, cp, _sz]
+        L.ref_archive_fetch.argtypes = [C.c_void_p, _sz]
+        L.ref_archive_decompress.argtypes = [C.c_void_p, _sz, _D, _sz, _SZ, _SZ, cp, _sz]
+        L.ref_archive_info.argtypes = [C.c_void_p, _sz, cp, _sz, cp, _sz]
+        L.ref_crc32.argtypes = [C.c_void_p, _sz]
+        L.ref_crc32.restype = C.c_uint32
         self.lib = L
+
+    # ---- archive codec (proj/src/archive.cpp; CLI batch compress) ----------------
+    def compress_field(self, a, dims, blocks, strides, rank=0, tol=0.0, periodic=None, qoi="",
+                       provenance=""):
+        """The CLI's batch compression of a structured field + encode() -> bytes."""
+        a = _f64(a)
+        m, n = a.shape
+        nax = len(dims)
+        d, p, s, _ = _Port._spec(dims, strides, periodic)
+        b = (C.c_size_t * nax)(*blocks)
+        nb = C.c_size_t(0)
+        self._call(self.lib.ref_compress_field, _dp(a), m, n, d, p, nax, b, s, int(rank or 0),
+                   float(tol or 0.0), qoi.encode(), provenance.encode(), C.byref(nb))
+        out = np.empty(nb.value, dtype=np.uint8)
+        self.lib.ref_archive_fetch(out.ctypes.data, nb.value)
+        return out.tobytes()
+
+    def archive_decompress(self, data):
+        b = np.frombuffer(bytes(data), dtype=np.uint8)
+        m, n = C.c_size_t(0), C.c_size_t(0)
+        self._call(self.lib.ref_archive_decompress, b.ctypes.data, b.size, None, 0, C.byref(m),
+                   C.byref(n))
+        out = np.empty((m.value, n.value), order="F")
+        self._call(self.lib.ref_archive_decompress, b.ctypes.data, b.size, _dp(out), out.size,
+                   C.byref(m), C.byref(n))
+        return out
+
+    def archive_info(self, data):
+        b = np.frombuffer(bytes(data), dtype=np.uint8)
+        buf = C.create_string_buffer(1 << 20)
+        self._call(self.lib.ref_archive_info, b.ctypes.data, b.size, buf, 1 << 20)
+        return buf.value.decode()
+
+    def crc32(self, data):
+        b = np.frombuffer(bytes(data), dtype=np.uint8)
+        return int(self.lib.ref_crc32(b.ctypes.data if b.size else None, b.size))
 
     def spid(self, a, dims, strides, rank=None, tol=None, periodic=None, include_boundary=True):
         """spid::spid + reconstruct(SpidFactors) (proj/src/id.cpp:62-96): IdResult

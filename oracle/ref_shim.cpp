@@ -264,3 +264,107 @@ int ref_interp_apply(const std::size_t* dims, const int* periodic, const std::si
 }
 
 }  // extern "C"
+
+// ---- archive codec ---------------------------------------------
+#include "spid/archive.hpp"
+#include "spid/blocking.hpp"
+
+namespace {
+std::vector<std::uint8_t> g_archive;  // last archive produced (single-threaded tests)
+}  // namespace
+
+extern "C" {
+
+// The CLI's batch compress of a structured field (what proj/tools/spid_cli.cpp
+// does for `spid compress --chunk 0` on a structured grid): one spid() per
+// block of make_block_domains (blocking.cpp:31-104) with
+// SubsampleSpec::strided(local, strides, true), sorted union indices, coarse
+// flag = coarse_count < block rows; then encode() (archive.cpp:193-212).
+// The bytes stay in g_archive; ref_archive_fetch copies them out.
+int ref_compress_field(const double* a, std::size_t m, std::size_t n, const std::size_t* dims,
+                       const int* periodic, std::size_t naxes, const std::size_t* blocks,
+                       const std::size_t* strides, std::size_t rank, double tol,
+                       const char* qoi, const char* provenance, std::size_t* nbytes, char* err,
+                       std::size_t errlen) {
+    try {
+        std::vector<std::size_t> d(dims, dims + naxes), b(blocks, blocks + naxes),
+            s(strides, strides + naxes);
+        std::vector<bool> p(naxes);
+        for (std::size_t i = 0; i < naxes; ++i) p[i] = periodic[i] != 0;
+        const spid::GridGeom grid = spid::GridGeom::structured(d, p);
+        const DenseMatrix am = from_ptr(a, m, n);
+        const auto rule = rank > 0 ? spid::RankRule::fixed(rank) : spid::RankRule::tolerance(tol);
+
+        spid::Archive ar;
+        ar.meta.grid = grid;
+        ar.meta.blocks_per_axis = b;
+        ar.meta.time_chunk = 0;
+        ar.meta.strides = s;
+        ar.meta.include_boundary = true;
+        ar.meta.mode = "batch";
+        ar.meta.rank_rule_mode = rank > 0 ? "fixed" : "tolerance";
+        ar.meta.rank_k = rank;
+        ar.meta.rank_tol = rank > 0 ? 0.0 : tol;
+        ar.meta.interp_recipe = "strided-multilinear";
+        ar.meta.qoi = qoi ? qoi : "";
+        ar.meta.m = m;
+        ar.meta.n = n;
+        ar.meta.provenance = provenance ? provenance : "";
+        for (const auto& dom : spid::make_block_domains(grid, b)) {
+            const auto spec = spid::SubsampleSpec::strided(dom.local, s, true);
+            spid::SpidFactors f = spid::spid(spid::select_rows(am, dom.rows), spec, rule);
+            std::vector<std::size_t> uni = f.base.skeleton_indices;
+            std::sort(uni.begin(), uni.end());
+            ar.blocks.push_back({std::move(uni), f.base.skeleton_indices, std::move(f.base.skeleton),
+                                 std::move(f.base.coeffs), spec.coarse_count() < dom.rows.size()});
+        }
+        g_archive = spid::encode(ar);
+        *nbytes = g_archive.size();
+        return 0;
+    } catch (const spid::Error& e) {
+        return fail(e, err, errlen);
+    }
+}
+
+int ref_archive_fetch(std::uint8_t* out, std::size_t cap) {
+    if (cap < g_archive.size()) return 1;
+    std::memcpy(out, g_archive.data(), g_archive.size());
+    return 0;
+}
+
+// decode() + decompress() (archive.cpp:214-249, 281-303) into an m x n buffer.
+int ref_archive_decompress(const std::uint8_t* bytes, std::size_t nbytes, double* out,
+                           std::size_t cap, std::size_t* m, std::size_t* n, char* err,
+                           std::size_t errlen) {
+    try {
+        const spid::Archive ar = spid::decode(std::vector<std::uint8_t>(bytes, bytes + nbytes));
+        const DenseMatrix r = spid::decompress(ar);
+        *m = r.rows();
+        *n = r.cols();
+        if (out && r.entry_count() <= cap)
+            std::memcpy(out, r.data(), r.entry_count() * sizeof(double));
+        return 0;
+    } catch (const spid::Error& e) {
+        return fail(e, err, errlen);
+    }
+}
+
+// archive_info_json (archive.cpp:260-268), for the info surface.
+int ref_archive_info(const std::uint8_t* bytes, std::size_t nbytes, char* out, std::size_t cap,
+                     char* err, std::size_t errlen) {
+    try {
+        const std::string s =
+            spid::archive_info_json(spid::decode(std::vector<std::uint8_t>(bytes, bytes + nbytes)));
+        if (s.size() + 1 > cap) return fail(spid::Error("InvalidArgument", "cap"), err, errlen);
+        std::memcpy(out, s.c_str(), s.size() + 1);
+        return 0;
+    } catch (const spid::Error& e) {
+        return fail(e, err, errlen);
+    }
+}
+
+std::uint32_t ref_crc32(const std::uint8_t* data, std::size_t length) {
+    return spid::crc32(data, length);
+}
+
+}  // extern "C"

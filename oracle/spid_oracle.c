@@ -379,7 +379,7 @@ int orc_row_indices(const size_t* dims, const int* periodic, const size_t* strid
     size_t ax[3][4096], na[3] = {1, 1, 1}, d[3] = {1, 1, 1};
     ax[1][0] = ax[2][0] = 0;
     for (size_t a = 0; a < naxes; ++a) {
-        if (dims[a] < 2 || dims[a] > 4096 || strides[a] < 1) return SPID_BAD_SUBSAMPLE_SPEC;
+        if (dims[a] < 1 || dims[a] > 4096 || strides[a] < 1) return SPID_BAD_SUBSAMPLE_SPEC; /* structured_block: >= 1 */
         d[a] = dims[a];
         na[a] = axis_coarse(dims[a], strides[a], periodic[a], incl, ax[a]);
     }
@@ -439,7 +439,7 @@ int orc_interp_apply(const size_t* dims, const int* periodic, const size_t* stri
                      int incl, const double* coarse, size_t k, double* fine) {
     size_t ax[3][4096], na[3] = {1, 1, 1}, d[3] = {1, 1, 1};
     for (size_t a = 0; a < naxes; ++a) {
-        if (dims[a] < 2 || dims[a] > 4096 || strides[a] < 1) return SPID_BAD_SUBSAMPLE_SPEC;
+        if (dims[a] < 1 || dims[a] > 4096 || strides[a] < 1) return SPID_BAD_SUBSAMPLE_SPEC; /* structured_block: >= 1 */
         d[a] = dims[a];
         na[a] = axis_coarse(dims[a], strides[a], periodic[a], incl, ax[a]);
     }

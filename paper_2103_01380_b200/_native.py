@@ -62,12 +62,35 @@ def grid_spec(dims, strides, periodic=None, include_boundary=True, nqoi=1) -> Gr
                     (C.c_int64 * 3)(*pad(strides, 1)), (C.c_int32 * 3)(*pad(per, 0)), nqoi)
 
 
+ARCHIVE_EXACT, ARCHIVE_SKETCH = 0, 1
+
+
+class ArchiveSpec(C.Structure):
+    _fields_ = [("naxes", C.c_int32), ("mode", C.c_int32), ("dims", C.c_int64 * 3),
+                ("periodic", C.c_int32 * 3), ("reserved", C.c_int32),
+                ("blocks_per_axis", C.c_int64 * 3), ("strides", C.c_int64 * 3),
+                ("ell", C.c_int64), ("seed", C.c_uint64), ("qoi", C.c_char_p),
+                ("provenance", C.c_char_p)]
+
+
+def archive_spec(dims, blocks, strides, periodic=None, mode=ARCHIVE_EXACT, ell=0, seed=0,
+                 qoi="", provenance="") -> ArchiveSpec:
+    nax = len(dims)
+    per = [int(bool(x)) for x in periodic] if periodic else [0] * nax
+    pad = lambda v, f: list(v) + [f] * (3 - nax)  # noqa: E731
+    return ArchiveSpec(nax, mode, (C.c_int64 * 3)(*pad(dims, 1)), (C.c_int32 * 3)(*pad(per, 0)), 0,
+                       (C.c_int64 * 3)(*pad(blocks, 1)), (C.c_int64 * 3)(*pad(strides, 1)), ell,
+                       seed, qoi.encode(), provenance.encode())
+
+
 _vp = C.c_void_p
 _i64 = C.c_int64
 _H = C.c_void_p
 _RR = C.POINTER(RankRule)
 _OM = C.POINTER(Omega)
 _GS = C.POINTER(GridSpec)
+_AS = C.POINTER(ArchiveSpec)
+_pi64 = C.POINTER(C.c_int64)
 
 # name -> (restype, argtypes)
 _SIGS = {
@@ -104,6 +127,12 @@ _SIGS = {
     "spidgpu_compression_factor": (C.c_int, [_i64, _i64, _i64, C.POINTER(C.c_double)]),
     "spidgpu_compress_host": (C.c_int, [_H, _vp, _i64, _i64, _i64, _i64, _OM, _RR, _i64, _i64,
                                         _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "spidgpu_crc32": (C.c_int, [_H, _vp, _i64, C.c_int32, C.POINTER(C.c_uint32)]),
+    "spidgpu_archive_compress": (C.c_int, [_H, _vp, _i64, _i64, _i64, C.c_int32, _AS, _RR, _pi64]),
+    "spidgpu_archive_fetch": (C.c_int, [_H, _vp, _i64]),
+    "spidgpu_archive_shape": (C.c_int, [_vp, _i64, _pi64, _pi64, _pi64]),
+    "spidgpu_archive_info": (C.c_int, [_H, _vp, _i64, _vp, _i64, _pi64]),
+    "spidgpu_archive_decompress": (C.c_int, [_H, _vp, _i64, _vp, _i64, C.c_int32]),
     "spidgpu_field_generate": (C.c_int, [_H, C.POINTER(FieldSpec), _i64, _i64, _vp, _vp, _i64,
                                          _i64, _vp]),
     "spidgpu_row_indices": (C.c_int, [_GS, _vp, _i64, C.POINTER(C.c_int64)]),

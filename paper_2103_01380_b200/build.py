@@ -3,7 +3,9 @@
     python -m paper_2103_01380_b200.build [--force] [-v]
 
 Every .cu under csrc/ is compiled for sm_100a only
-(-gencode arch=compute_100a,code=sm_100a) with -lineinfo, then linked into
+(-gencode arch=compute_100a,code=sm_100a) with -lineinfo; the host-only .cpp
+files (archive metadata JSON, via the nlohmann/json single header that ships
+in this image's cudnn_frontend wheel) with g++; everything is linked into
 paper_2103_01380_b200/lib/libspidgpu.so (static cudart; the TMA encoder is
 resolved through cudaGetDriverEntryPoint, so no -lcuda). The .so is
 git-ignored but travels to the GPU box with the gpurun snapshot.
@@ -30,6 +32,22 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-re
          "-Xptxas", "-warn-spills", f"-I{INCLUDE}"]
 
 
+CXX = os.environ.get("CXX", shutil.which("g++") or "g++")
+
+
+def _nlohmann_dir() -> str:
+    """Directory holding nlohmann/json's single-header json.hpp (3.11.3)."""
+    import sysconfig
+    cands = [os.environ.get("SPIDGPU_JSON_DIR", "")]
+    for key in ("purelib", "platlib"):
+        cands.append(os.path.join(sysconfig.get_paths()[key], "include", "cudnn_frontend",
+                                  "thirdparty", "nlohmann"))
+    for c in cands:
+        if c and os.path.exists(os.path.join(c, "json.hpp")):
+            return c
+    raise RuntimeError("nlohmann json.hpp not found (set SPIDGPU_JSON_DIR)")
+
+
 def _deps():
     return sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) +
                   glob.glob(os.path.join(INCLUDE, "*.h")))
@@ -43,21 +61,26 @@ def _stale(target, inputs):
 
 
 def _compile(src, verbose):
-    obj = os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
+    base, ext = os.path.splitext(os.path.basename(src))
+    obj = os.path.join(OBJ, base + (".o" if ext == ".cu" else ".cpp.o"))
     if not _stale(obj, [src] + _deps()):
         return obj, None
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
+    if ext == ".cpp":
+        cmd = [CXX, "-O3", "-std=c++17", "-fPIC", f"-I{INCLUDE}", f"-I{_nlohmann_dir()}", "-c", src,
+               "-o", obj]
+    else:
+        cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+        raise RuntimeError(f"compile failed for {src}:\n{r.stdout}\n{r.stderr}")
     return obj, (r.stdout + r.stderr).strip() or None
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
-    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
     if force:
         for f in glob.glob(os.path.join(OBJ, "*.o")):
             os.remove(f)

@@ -15,78 +15,12 @@
 #include <vector>
 
 #include "../../include/spidgpu.h"
+#include "context.h"
 #include "kernels.h"
 
 using namespace spidgpu;
 
-namespace {
-
-// ---- device buffers --------------------------------------------------------
-struct DevBuf {
-    void* ptr = nullptr;
-    size_t bytes = 0;
-    cudaError_t ensure(size_t need, cudaStream_t stream) {
-        if (need <= bytes) return cudaSuccess;
-        if (ptr) {
-            cudaError_t e = cudaStreamSynchronize(stream);
-            if (e != cudaSuccess) return e;
-            cudaFree(ptr);
-            ptr = nullptr;
-            bytes = 0;
-        }
-        size_t want = std::max(need, bytes * 3 / 2);
-        cudaError_t e = cudaMalloc(&ptr, want);
-        if (e != cudaSuccess) {
-            ptr = nullptr;
-            return e;
-        }
-        bytes = want;
-        return cudaSuccess;
-    }
-    template <class T>
-    T* as() const {
-        return static_cast<T*>(ptr);
-    }
-    void release() {
-        if (ptr) cudaFree(ptr);
-        ptr = nullptr;
-        bytes = 0;
-    }
-};
-
-// One workspace set per concurrently used stream.
-struct Workspace {
-    DevBuf partial, rws, wws, r11ws, ybuf, vpart, flag;
-    // host-API / compress_host staging
-    DevBuf a, omega, idx, coeffs, skel, rank, resid, status, err2, ref2, rows, out, pivots, r, q;
-    void release() {
-        for (DevBuf* b : {&partial, &rws, &wws, &r11ws, &ybuf, &vpart, &flag, &a, &omega, &idx, &coeffs,
-                          &skel, &rank, &resid, &status, &err2, &ref2, &rows, &out, &pivots, &r,
-                          &q})
-            b->release();
-    }
-};
-
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-}  // namespace
-
-struct spidgpu_context {
-    int device = 0;
-    int num_sms = 148;
-    Workspace ws[3];
-    cudaStream_t lanes[2] = {nullptr, nullptr};
-    cudaEvent_t ev[2] = {nullptr, nullptr};
-    EncodeTiledFn encode = nullptr;
-    int64_t launches = 0;
-    std::string last_error;
-    bool force_generic_cpqr = false;  // tests: exercise the shared/global-W kernel too
-};
-
-namespace {
+namespace spidgpu {
 
 thread_local std::string g_create_error;
 
@@ -98,18 +32,6 @@ int fail(spidgpu_handle h, int code, const std::string& msg) {
 int cuda_fail(spidgpu_handle h, cudaError_t e, const char* where) {
     return fail(h, SPID_CUDA_ERROR, std::string(where) + ": " + cudaGetErrorString(e));
 }
-
-#define CK(h, expr)                                              \
-    do {                                                         \
-        cudaError_t _e = (expr);                                 \
-        if (_e != cudaSuccess) return cuda_fail((h), _e, #expr); \
-    } while (0)
-
-struct RuleInfo {
-    int status = SPID_OK;       // immediate (BadRankRule, InvalidArgument)
-    int pre_status = SPID_OK;   // batch-uniform kernel-reported (RankUnreachable)
-    int64_t step_limit = 0;
-};
 
 // RankRule validation (proj/include/spid/qr.hpp:16-24) and step limits
 // (proj/src/qr.cpp:22-25, 37-38, 53-54).
@@ -371,13 +293,6 @@ int do_compress(spidgpu_handle h, Workspace& ws, const double* A, int64_t m, int
 }
 
 // ---- host-API helpers ---------------------------------------------------------
-template <class T>
-int to_dev(spidgpu_handle h, DevBuf& buf, const T* src, size_t count, cudaStream_t st) {
-    CK(h, buf.ensure(sizeof(T) * std::max<size_t>(count, 1), st));
-    if (count) CK(h, cudaMemcpyAsync(buf.ptr, src, sizeof(T) * count, cudaMemcpyHostToDevice, st));
-    return SPID_OK;
-}
-
 bool all_finite_host_free() { return true; }
 
 // Copy an m x n host matrix into a device buffer with an even leading
@@ -468,14 +383,14 @@ std::vector<double> make_modes(uint64_t seed, int count, double kmin, double kma
     return out;
 }
 
-}  // namespace
+}  // namespace spidgpu
 
-namespace {
+namespace spidgpu {
 
 // ---- SPID grid specs ----------------------------------------------------------------
 // Validation of SubsampleSpec::strided / GridGeom::structured (grid.cpp:7-20, 62-75).
 int spec_to_dev(spidgpu_handle h, const spidgpu_grid_spec* sp, GridSpecDev* g, int64_t* P,
-                int64_t* Pc) {
+                int64_t* Pc, int min_dim) {
     if (!sp) return fail(h, SPID_INVALID_ARGUMENT, "null grid spec");
     if (sp->naxes < 1 || sp->naxes > 3) return fail(h, SPID_BAD_GRID_GEOM, "structured grids have 1 to 3 axes");
     if (sp->nqoi < 1) return fail(h, SPID_BAD_SUBSAMPLE_SPEC, "nqoi must be >= 1");
@@ -486,8 +401,9 @@ int spec_to_dev(spidgpu_handle h, const spidgpu_grid_spec* sp, GridSpecDev* g, i
     *Pc = 1;
     for (int ax = 0; ax < 3; ++ax) {
         if (ax < sp->naxes) {
-            if (sp->dims[ax] < 2 || sp->dims[ax] > (1 << 20))
-                return fail(h, SPID_BAD_GRID_GEOM, "each structured axis needs at least 2 points");
+            if (sp->dims[ax] < min_dim || sp->dims[ax] > (1 << 20))
+                return fail(h, SPID_BAD_GRID_GEOM, min_dim > 1 ? "each structured axis needs at least 2 points"
+                                                               : "block axis needs at least 1 point");
             if (sp->strides[ax] < 1) return fail(h, SPID_BAD_SUBSAMPLE_SPEC, "strides must be >= 1");
             g->dims[ax] = static_cast<int>(sp->dims[ax]);
             g->strides[ax] = static_cast<int>(sp->strides[ax]);
@@ -531,7 +447,7 @@ std::vector<int64_t> spec_rows(const GridSpecDev& g, int64_t P) {
     return rows;
 }
 
-}  // namespace
+}  // namespace spidgpu
 
 // =====================================================================
 extern "C" {
@@ -556,6 +472,14 @@ const char* spidgpu_status_name(int status) {
         case SPID_EMPTY_SKETCH: return "EmptySketch";
         case SPID_EXTRAPOLATION_REQUIRED: return "ExtrapolationRequired";
         case SPID_BAD_GRID_GEOM: return "BadGridGeom";
+        case SPID_BLOCK_TOO_SMALL: return "BlockTooSmall";
+        case SPID_BAD_MAGIC: return "BadMagic";
+        case SPID_VERSION_UNSUPPORTED: return "VersionUnsupported";
+        case SPID_TRUNCATED_PAYLOAD: return "TruncatedPayload";
+        case SPID_CHECKSUM_MISMATCH: return "ChecksumMismatch";
+        case SPID_COVERAGE_GAP: return "CoverageGap";
+        case SPID_UNSTRUCTURED_NO_INTERP: return "UnstructuredNoInterp";
+        case SPID_BAD_STREAM_CONFIG: return "BadStreamConfig";
         case SPID_CUDA_ERROR: return "CudaError";
         case SPID_INVALID_ARGUMENT: return "InvalidArgument";
         case SPID_SHAPE_UNSUPPORTED: return "ShapeUnsupported";

@@ -1,0 +1,382 @@
+// archive.cu -- device side of the archive codec (proj/src/archive.cpp).
+//
+// The archive of a field is assembled in HBM and leaves the GPU with one
+// device-to-host copy:
+//   gather_block_rows   B_b = A(rows of block b restricted to the coarse set J)
+//                       -- select_rows + subsample of compress_structured_batch
+//   sort_union          union_indices = sorted skeleton indices
+//   pack_blocks         block sections: u64 length | payload | (crc), payload =
+//                       u8 coarse | u64 array union | u64 array skeleton idx |
+//                       f64 matrix skeleton | f64 matrix coeffs
+//                       (archive.cpp:100-116, 193-212), all little-endian
+//   crc_sections        CRC-32 of every section payload (archive.cpp:83-98)
+// and decompress (archive.cpp:281-303) runs as
+//   unpack_blocks       f64 matrices of each section -> padded batch buffers
+//   (interp lift of coarse skeletons, interp.cu)
+//   recon_scatter       out(rows_b, :) = F_b * C_b, the reference matmul's
+//                       j-k-i order with its zero skip (dense_matrix.cpp:
+//                       38-53), rounded per operation -> bit-identical, written
+//                       straight into the assembled matrix (blocking.cpp:219-241).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace spidgpu {
+
+namespace {
+
+constexpr uint32_t kPolyR = 0xEDB88320u;
+
+__device__ inline uint32_t multmodp_d(uint32_t a, uint32_t b) {
+    uint32_t m = 1u << 31, p = 0;
+    for (;;) {
+        if (a & m) {
+            p ^= b;
+            if ((a & (m - 1)) == 0) break;
+        }
+        m >>= 1;
+        b = (b & 1) ? (b >> 1) ^ kPolyR : b >> 1;
+    }
+    return p;
+}
+
+__device__ inline uint32_t xpow8_d(uint64_t nbytes) {
+    uint32_t sq = 1u << 30;
+    for (int i = 0; i < 3; ++i) sq = multmodp_d(sq, sq);
+    uint32_t p = 1u << 31;
+    while (nbytes) {
+        if (nbytes & 1) p = multmodp_d(sq, p);
+        sq = multmodp_d(sq, sq);
+        nbytes >>= 1;
+    }
+    return p;
+}
+
+__global__ void gather_block_rows_kernel(const double* __restrict__ A, int64_t lda,
+                                         const int64_t* __restrict__ rel, int64_t nrows,
+                                         const int64_t* __restrict__ bases, int64_t nb, int64_t n,
+                                         double* __restrict__ B, int64_t ldb, int64_t strideB) {
+    const int64_t total = nb * n * nrows;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = e % nrows;
+        const int64_t j = (e / nrows) % n;
+        const int64_t b = e / (nrows * n);
+        B[b * strideB + j * ldb + i] = __ldg(A + j * lda + bases[b] + rel[i]);
+    }
+}
+
+__global__ void sort_union_kernel(const int64_t* __restrict__ idx, int64_t kcap,
+                                  const int64_t* __restrict__ rank, int64_t nb,
+                                  int64_t* __restrict__ uni) {
+    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (b >= nb) return;
+    const int64_t k = rank[b];
+    const int64_t* src = idx + b * kcap;
+    int64_t* dst = uni + b * kcap;
+    for (int64_t t = 0; t < k; ++t) {  // insertion sort, k <= a few hundred
+        const int64_t v = src[t];
+        int64_t u = t;
+        while (u > 0 && dst[u - 1] > v) {
+            dst[u] = dst[u - 1];
+            --u;
+        }
+        dst[u] = v;
+    }
+}
+
+__device__ __forceinline__ void put_u64(uint8_t* p, uint64_t v) {
+#pragma unroll
+    for (int b = 0; b < 8; ++b) p[b] = static_cast<uint8_t>(v >> (8 * b));
+}
+
+__device__ __forceinline__ uint64_t get_u64(const uint8_t* p) {
+    uint64_t v = 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) v |= static_cast<uint64_t>(__ldg(p + b)) << (8 * b);
+    return v;
+}
+
+// One thread per 8-byte item of a section (item 1 is the coarse byte).
+__global__ void pack_blocks_kernel(const PackBlock* __restrict__ blocks, int64_t nblocks,
+                                   uint8_t* __restrict__ out) {
+    for (int64_t b = blockIdx.y; b < nblocks; b += gridDim.y) {
+        const PackBlock d = blocks[b];
+        const int64_t k = d.k, mck = d.mc * d.k, kn = d.k * d.n;
+        const int64_t items = 8 + 2 * k + mck + kn;
+        const int64_t payload = 49 + 16 * k + 8 * mck + 8 * kn;
+        for (int64_t it = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; it < items;
+             it += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            uint8_t* sec = out + d.sec_off;
+            if (it == 0) {
+                put_u64(sec, static_cast<uint64_t>(payload));
+                continue;
+            }
+            if (it == 1) {
+                sec[8] = d.coarse ? 1 : 0;
+                continue;
+            }
+            const int64_t q = it - 2;
+            uint64_t v;
+            if (q == 0 || q == k + 1) {
+                v = static_cast<uint64_t>(k);
+            } else if (q <= k) {
+                v = static_cast<uint64_t>(d.uni[q - 1]);
+            } else if (q <= 2 * k + 1) {
+                v = static_cast<uint64_t>(d.sel[q - k - 2]);
+            } else if (q == 2 * k + 2) {
+                v = static_cast<uint64_t>(d.mc);
+            } else if (q == 2 * k + 3) {
+                v = static_cast<uint64_t>(k);
+            } else if (q < 2 * k + 4 + mck) {
+                const uint32_t e = static_cast<uint32_t>(q - (2 * k + 4));
+                const uint32_t mc = static_cast<uint32_t>(d.mc);
+                v = __double_as_longlong(__ldg(d.skel + static_cast<int64_t>(e / mc) * d.ld_s + e % mc));
+            } else if (q == 2 * k + 4 + mck) {
+                v = static_cast<uint64_t>(k);
+            } else if (q == 2 * k + 5 + mck) {
+                v = static_cast<uint64_t>(d.n);
+            } else {
+                const uint32_t e = static_cast<uint32_t>(q - (2 * k + 6 + mck));
+                const uint32_t kk = static_cast<uint32_t>(k);
+                v = __double_as_longlong(__ldg(d.coeffs + static_cast<int64_t>(e / kk) * d.ld_c + e % kk));
+            }
+            put_u64(sec + 9 + 8 * q, v);
+        }
+    }
+}
+
+// Raw CRC (state 0, no final xor) of bytes [lo, hi).
+__device__ uint32_t crc_raw_range(const uint8_t* __restrict__ data, int64_t lo, int64_t hi,
+                                  const uint32_t (*T)[256]) {
+    uint32_t c = 0;
+    int64_t p = lo;
+    while (p < hi && (reinterpret_cast<uintptr_t>(data + p) & 7)) {
+        c = T[0][(c ^ __ldg(data + p)) & 0xff] ^ (c >> 8);
+        ++p;
+    }
+    for (; p + 8 <= hi; p += 8) {
+        const uint64_t w = __ldg(reinterpret_cast<const unsigned long long*>(data + p));
+        c ^= static_cast<uint32_t>(w);
+        const uint32_t h = static_cast<uint32_t>(w >> 32);
+        c = T[7][c & 0xff] ^ T[6][(c >> 8) & 0xff] ^ T[5][(c >> 16) & 0xff] ^ T[4][c >> 24] ^
+            T[3][h & 0xff] ^ T[2][(h >> 8) & 0xff] ^ T[1][(h >> 16) & 0xff] ^ T[0][h >> 24];
+    }
+    for (; p < hi; ++p) c = T[0][(c ^ __ldg(data + p)) & 0xff] ^ (c >> 8);
+    return c;
+}
+
+constexpr int kCrcThreads = 256;
+
+// One CTA per section: 256 contiguous end-aligned chunks, slice-by-8 each,
+// combined through x^(8*len) shifts (crc.cu explains the identities).
+__global__ void __launch_bounds__(kCrcThreads)
+    crc_sections_kernel(const uint8_t* __restrict__ data, const CrcSection* __restrict__ secs,
+                        int64_t nsec, uint32_t* __restrict__ crc_out, uint8_t* write_back) {
+    __shared__ uint32_t T[8][256];
+    __shared__ uint32_t part[kCrcThreads / kWarp];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        uint32_t c = i;
+        for (int b = 0; b < 8; ++b) c = (c & 1) ? (c >> 1) ^ kPolyR : c >> 1;
+        T[0][i] = c;
+    }
+    __syncthreads();
+    for (int t = 1; t < 8; ++t) {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x)
+            T[t][i] = (T[t - 1][i] >> 8) ^ T[0][T[t - 1][i] & 0xff];
+        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t s = blockIdx.x; s < nsec; s += gridDim.x) {
+        const int64_t begin = secs[s].begin, len = secs[s].len, end = begin + len;
+        const int64_t C = len > 0 ? (len + kCrcThreads - 1) / kCrcThreads : 1;
+        int64_t lo = end - (kCrcThreads - threadIdx.x) * C;
+        const int64_t hi = lo + C;
+        if (lo < begin) lo = begin;
+        uint32_t c = lo < hi ? crc_raw_range(data, lo, hi, T) : 0u;
+        uint32_t X = xpow8_d(static_cast<uint64_t>(C));  // shift past one chunk
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            const uint32_t other = __shfl_down_sync(0xffffffffu, c, 1 << j);
+            if ((lane & ((2 << j) - 1)) == 0) c = multmodp_d(X, c) ^ other;
+            X = multmodp_d(X, X);
+        }
+        if (lane == 0) part[warp] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t acc = part[0];
+            for (int w = 1; w < kCrcThreads / kWarp; ++w) acc = multmodp_d(X, acc) ^ part[w];
+            const uint32_t crc = ~(acc ^ multmodp_d(xpow8_d(static_cast<uint64_t>(len)), 0xFFFFFFFFu));
+            crc_out[s] = crc;
+            if (write_back) {
+#pragma unroll
+                for (int b = 0; b < 4; ++b) write_back[end + b] = static_cast<uint8_t>(crc >> (8 * b));
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void unpack_blocks_kernel(const uint8_t* __restrict__ bytes,
+                                     const UnpackBlock* __restrict__ blocks, int64_t nblocks) {
+    for (int64_t b = blockIdx.y; b < nblocks; b += gridDim.y) {
+        const UnpackBlock d = blocks[b];
+        const int64_t mck = d.mc * d.k, total = mck + d.k * d.n;
+        for (int64_t it = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; it < total;
+             it += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            if (it < mck) {
+                const int64_t col = it / d.mc, row = it % d.mc;
+                d.skel[col * d.ld_s + row] = __longlong_as_double(get_u64(bytes + d.skel_off + 8 * it));
+            } else {
+                const int64_t e = it - mck;
+                const int64_t col = e / d.k, row = e % d.k;
+                d.coeffs[col * d.ld_c + row] =
+                    __longlong_as_double(get_u64(bytes + d.coef_off + 8 * e));
+            }
+        }
+    }
+}
+
+constexpr int kReconRows = 128;
+constexpr int kReconCols = 64;
+constexpr int kReconNJ = 8;
+
+// out(bases[b] + rel[i], j) = sum_t F_b(i, t) * C_b(t, j) in the reference
+// matmul's order: t ascending, products with C == 0 skipped, every multiply
+// and add rounded on its own.
+__global__ void __launch_bounds__(kReconRows)
+    recon_scatter_kernel(const double* __restrict__ F, int64_t ldf, int64_t strideF,
+                         const double* __restrict__ Cm, int64_t kcap, int64_t strideC,
+                         const int64_t* __restrict__ rank, int64_t mb, int64_t n,
+                         const int64_t* __restrict__ rel, const int64_t* __restrict__ bases,
+                         double* __restrict__ out, int64_t ldo) {
+    extern __shared__ double cs[];  // [kcap][kReconCols]
+    const int64_t b = blockIdx.y;
+    const int64_t i = blockIdx.x * static_cast<int64_t>(kReconRows) + threadIdx.x;
+    const int k = static_cast<int>(rank[b]);
+    const double* Fb = F + b * strideF;
+    const double* Cb = Cm + b * strideC;
+    const int64_t orow = i < mb ? bases[b] + rel[i] : 0;
+    for (int64_t c0 = 0; c0 < n; c0 += kReconCols) {
+        const int ncol = static_cast<int>(n - c0 < kReconCols ? n - c0 : kReconCols);
+        __syncthreads();
+        for (int e = threadIdx.x; e < k * kReconCols; e += kReconRows) {
+            const int t = e / kReconCols, jj = e % kReconCols;
+            cs[t * kReconCols + jj] = jj < ncol ? Cb[(c0 + jj) * kcap + t] : 0.0;
+        }
+        __syncthreads();
+        if (i >= mb) continue;
+        for (int j0 = 0; j0 < ncol; j0 += kReconNJ) {
+            double acc[kReconNJ];
+#pragma unroll
+            for (int u = 0; u < kReconNJ; ++u) acc[u] = 0.0;
+            for (int t = 0; t < k; ++t) {
+                const double a = __ldg(Fb + t * ldf + i);
+#pragma unroll
+                for (int u = 0; u < kReconNJ; ++u) {
+                    const double bv = cs[t * kReconCols + j0 + u];
+                    if (bv != 0.0) acc[u] = add_rn(acc[u], mul_rn(a, bv));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kReconNJ; ++u)
+                if (j0 + u < ncol) out[(c0 + j0 + u) * ldo + orow] = acc[u];
+        }
+    }
+}
+
+__global__ void nonfinite_blocks_kernel(const double* __restrict__ A, int64_t lda, int64_t m,
+                                        int64_t n, BlockGridDev g, int32_t* __restrict__ flags) {
+    const int64_t total = m * n;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = e % m, j = e / m;
+        const double v = A[j * lda + r];
+        if (isfinite(v)) continue;
+        int64_t rem = r, blk = 0, mul = 1;
+        for (int ax = 0; ax < g.naxes; ++ax) {
+            const int64_t coord = rem % g.dims[ax];
+            rem /= g.dims[ax];
+            int64_t seg = coord / g.seg_base[ax];
+            if (seg >= g.seg_count[ax]) seg = g.seg_count[ax] - 1;
+            blk += seg * mul;
+            mul *= g.seg_count[ax];
+        }
+        if (rem == 0) atomicExch(flags + blk, 1);  // rows past the grid are ignored
+    }
+}
+
+int grid_for(int64_t work, int per) {
+    int64_t g = (work + per - 1) / per;
+    if (g > 148 * 16) g = 148 * 16;
+    return static_cast<int>(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+cudaError_t launch_gather_block_rows(const double* A, int64_t lda, const int64_t* rel,
+                                     int64_t nrows, const int64_t* bases, int64_t nb, int64_t n,
+                                     double* B, int64_t ldb, int64_t strideB, cudaStream_t st) {
+    gather_block_rows_kernel<<<grid_for(nb * n * nrows, 256), 256, 0, st>>>(A, lda, rel, nrows, bases,
+                                                                            nb, n, B, ldb, strideB);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sort_union(const int64_t* idx, int64_t kcap, const int64_t* rank, int64_t nb,
+                              int64_t* uni, cudaStream_t st) {
+    sort_union_kernel<<<static_cast<unsigned>((nb + 127) / 128), 128, 0, st>>>(idx, kcap, rank, nb, uni);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_blocks(const PackBlock* blocks, int64_t nblocks, int64_t max_items,
+                               uint8_t* out, cudaStream_t st) {
+    const unsigned gy = static_cast<unsigned>(nblocks < 65535 ? nblocks : 65535);
+    int64_t gx = (max_items + 255) / 256;
+    const int64_t cap = (148 * 32 + gy - 1) / gy;
+    if (gx > cap) gx = cap;
+    if (gx < 1) gx = 1;
+    pack_blocks_kernel<<<dim3(static_cast<unsigned>(gx), gy), 256, 0, st>>>(blocks, nblocks, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_crc_sections(const uint8_t* data, const CrcSection* secs, int64_t nsec,
+                                uint32_t* crc_out, uint8_t* write_back, cudaStream_t st) {
+    const int64_t g = nsec < 148 * 8 ? nsec : 148 * 8;
+    crc_sections_kernel<<<static_cast<unsigned>(g < 1 ? 1 : g), kCrcThreads, 0, st>>>(
+        data, secs, nsec, crc_out, write_back);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_blocks(const uint8_t* bytes, const UnpackBlock* blocks, int64_t nblocks,
+                                 int64_t max_items, cudaStream_t st) {
+    const unsigned gy = static_cast<unsigned>(nblocks < 65535 ? nblocks : 65535);
+    int64_t gx = (max_items + 255) / 256;
+    const int64_t cap = (148 * 32 + gy - 1) / gy;
+    if (gx > cap) gx = cap;
+    if (gx < 1) gx = 1;
+    unpack_blocks_kernel<<<dim3(static_cast<unsigned>(gx), gy), 256, 0, st>>>(bytes, blocks, nblocks);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_recon_scatter(const double* F, int64_t ldf, int64_t strideF, const double* C,
+                                 int64_t kcap, int64_t strideC, const int64_t* rank, int64_t nb,
+                                 int64_t mb, int64_t n, const int64_t* rel, const int64_t* bases,
+                                 double* out, int64_t ldo, cudaStream_t st) {
+    const size_t smem = sizeof(double) * static_cast<size_t>(kcap) * kReconCols;
+    if (smem > 200 * 1024 || nb > 65535) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(recon_scatter_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    const dim3 grid(static_cast<unsigned>((mb + kReconRows - 1) / kReconRows), static_cast<unsigned>(nb));
+    recon_scatter_kernel<<<grid, kReconRows, smem, st>>>(F, ldf, strideF, C, kcap, strideC, rank, mb,
+                                                         n, rel, bases, out, ldo);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_nonfinite_blocks(const double* A, int64_t lda, int64_t m, int64_t n,
+                                    const BlockGridDev& g, int32_t* flags, cudaStream_t st) {
+    nonfinite_blocks_kernel<<<grid_for(m * n, 256), 256, 0, st>>>(A, lda, m, n, g, flags);
+    return cudaGetLastError();
+}
+
+}  // namespace spidgpu

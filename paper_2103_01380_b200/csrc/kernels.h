@@ -138,6 +138,56 @@ cudaError_t launch_gather_coarse(const double* A, int64_t lda, int64_t strideA, 
                                  const int64_t* rank, int64_t batch, double* skel, int64_t ldskel,
                                  int64_t strideS, cudaStream_t stream);
 
+// ---- CRC-32 (crc.cu) -------------------------------------------------------
+cudaError_t launch_crc32(const uint8_t* data, int64_t nbytes, uint32_t* block_scratch,
+                         uint32_t* out, cudaStream_t stream);
+int64_t crc32_scratch_words(int64_t nbytes);
+
+// ---- archive codec (archive.cu) --------------------------------------------
+struct PackBlock {          // one block section of the archive
+    int64_t sec_off;        // archive offset of the section's u64 length field
+    int64_t k, mc, n;       // rank, skeleton rows, snapshot columns
+    int32_t coarse;
+    const int64_t* uni;     // sorted skeleton indices
+    const int64_t* sel;     // skeleton indices in selection order
+    const double* skel;     // mc x k, ld ld_s
+    int64_t ld_s;
+    const double* coeffs;   // k x n, ld ld_c
+    int64_t ld_c;
+};
+struct CrcSection {
+    int64_t begin, len;     // payload byte range; the CRC follows it
+};
+struct UnpackBlock {
+    int64_t skel_off, coef_off;  // archive offsets of the first f64 of each matrix
+    int64_t mc, k, n;
+    double* skel;                // destination mc x k, ld ld_s
+    int64_t ld_s;
+    double* coeffs;              // destination k x n, ld ld_c
+    int64_t ld_c;
+};
+struct BlockGridDev {       // make_block_domains segments per axis
+    int naxes;
+    int64_t dims[3], seg_base[3], seg_count[3];
+};
+cudaError_t launch_gather_block_rows(const double* A, int64_t lda, const int64_t* rel,
+                                     int64_t nrows, const int64_t* bases, int64_t nb, int64_t n,
+                                     double* B, int64_t ldb, int64_t strideB, cudaStream_t st);
+cudaError_t launch_sort_union(const int64_t* idx, int64_t kcap, const int64_t* rank, int64_t nb,
+                              int64_t* uni, cudaStream_t st);
+cudaError_t launch_pack_blocks(const PackBlock* blocks, int64_t nblocks, int64_t max_items,
+                               uint8_t* out, cudaStream_t st);
+cudaError_t launch_crc_sections(const uint8_t* data, const CrcSection* secs, int64_t nsec,
+                                uint32_t* crc_out, uint8_t* write_back, cudaStream_t st);
+cudaError_t launch_unpack_blocks(const uint8_t* bytes, const UnpackBlock* blocks, int64_t nblocks,
+                                 int64_t max_items, cudaStream_t st);
+cudaError_t launch_recon_scatter(const double* F, int64_t ldf, int64_t strideF, const double* C,
+                                 int64_t kcap, int64_t strideC, const int64_t* rank, int64_t nb,
+                                 int64_t mb, int64_t n, const int64_t* rel, const int64_t* bases,
+                                 double* out, int64_t ldo, cudaStream_t st);
+cudaError_t launch_nonfinite_blocks(const double* A, int64_t lda, int64_t m, int64_t n,
+                                    const BlockGridDev& g, int32_t* flags, cudaStream_t st);
+
 // ---- synthetic fields (fields.cu) ----------------------------------------
 struct FieldParams {
     int kind;

@@ -93,6 +93,59 @@ def main():
         cases[key + "_resid"] = np.array([f.residual_fro])
     np.savez_compressed(os.path.join(OUT, "reference_cases.npz"), **cases)
     print("wrote", len(cases), "arrays")
+    archive_cases(ref, port)
+
+
+def smooth_field(dims, n, seed):
+    """Deterministic smooth snapshots on a structured grid (rows = points,
+    axis 0 fastest): a few separable Fourier modes with decaying amplitudes,
+    each with its own temporal frequency, plus a little seeded noise."""
+    rng = np.random.default_rng(seed)
+    axes = np.meshgrid(*[np.arange(d) / d for d in dims], indexing="ij")
+    t = np.linspace(0.0, 1.0, n)
+    a = np.zeros((int(np.prod(dims)), n))
+    for mode in range(6):
+        ks = rng.integers(1, 3, size=len(dims))
+        ph = rng.uniform(0, 2 * np.pi, size=len(dims))
+        shape = np.ones_like(axes[0])
+        for ax, k, p in zip(axes, ks, ph):
+            shape = shape * np.sin(2 * np.pi * k * ax + p)
+        a += (0.5 ** mode) * np.outer(shape.ravel(order="F"), np.cos(2 * np.pi * (mode + 1) * t + mode))
+    return np.asfortranarray(a + 1e-6 * rng.standard_normal(a.shape))
+
+
+# (dims, blocks, strides, periodic, rank, tol, snapshots, input kind)
+ARCHIVE_CASES = [
+    ((10, 10), (2, 2), (2, 2), (1, 1), 1, 0.0, 20, "smooth"),
+    ((13, 11, 9), (3, 2, 2), (2, 3, 1), (0, 1, 0), 0, 1e-3, 15, "smooth"),
+    ((17,), (3,), (4,), (0,), 2, 0.0, 9, "seeded"),
+    ((12, 8), (1, 1), (1, 1), (1, 1), 4, 0.0, 10, "seeded"),
+    ((9, 7, 6), (9, 1, 2), (2, 2, 2), (0, 0, 0), 1, 0.0, 6, "seeded"),
+    ((12, 12, 12), (2, 2, 2), (2, 2, 2), (1, 1, 1), 5, 0.0, 16, "smooth"),
+    ((20, 14), (3, 2), (3, 2), (0, 0), 0, 1e-6, 12, "smooth"),
+]
+
+
+def archive_cases(ref, port):
+    """Archives of the CLI's batch compression (spid_cli.cpp:195-232 +
+    archive.cpp encode) and their decompress(), from the reference."""
+    cases = {}
+    for ci, (dims, blocks, strides, per, rank, tol, n, kind) in enumerate(ARCHIVE_CASES):
+        m = int(np.prod(dims))
+        a = smooth_field(dims, n, 77 + ci) if kind == "smooth" else port.seeded_matrix(m, n, 500 + ci)
+        data = ref.compress_field(a, dims, blocks, strides, rank=rank, tol=tol, periodic=per,
+                                  qoi=f"q{ci}", provenance="golden fixture")
+        out = ref.archive_decompress(data)
+        key = f"arc_{ci}"
+        cases[key + "_a"] = a
+        cases[key + "_params"] = np.array([len(dims), *dims, *blocks, *strides, *per, rank, n], dtype=np.int64)
+        cases[key + "_tol"] = np.array([tol])
+        cases[key + "_bytes"] = np.frombuffer(data, dtype=np.uint8).copy()
+        cases[key + "_out_sha"] = digest(out)
+        cases[key + "_info"] = np.frombuffer(ref.archive_info(data).encode(), dtype=np.uint8).copy()
+    cases["crc_kat"] = np.array([ref.crc32(b"123456789")], dtype=np.int64)
+    np.savez_compressed(os.path.join(OUT, "archive_cases.npz"), **cases)
+    print("wrote", len(cases), "archive arrays")
 
 
 if __name__ == "__main__":
