@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-quality", action="store_true")
+    ap.add_argument("--no-archive", action="store_true")
     return ap.parse_args()
 
 
@@ -364,6 +365,8 @@ def run_ours(args):
         line["quality_spid"] = quality_spid(eng, cfg, field, A, first, count, world, stream)
     if not args.no_e2e:
         line["e2e"] = e2e_measure(eng, cfg, A, first, count, rule, args, world)
+    if not args.no_archive and world == 1:
+        line["archive"] = archive_measure(cfg, A, args)
     if world > 1:
         dist.barrier()
     if rank == 0 and not args.no_cpu_baseline and world == 1:
@@ -495,6 +498,112 @@ def e2e_measure(eng, cfg, A, first, count, rule, args, world):
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "api": "spidgpu_compress_host (C ABI, pinned host buffers, 2 copy/compute lanes)",
             "steps": args.e2e_steps, "ms_per_step": sec * 1e3}
+
+
+def global_field(A, grid, block, qoi):
+    """QoI `qoi` of the block-major batch A [S, n, qois*b^3] as one structured
+    field (m = grid^3 rows, axis 0 fastest) in column-major layout, blocks in
+    make_block_domains order (proj/src/blocking.cpp:31-98)."""
+    import torch
+
+    S, n, _ = A.shape
+    b3 = block ** 3
+    nb = grid // block
+    ar = torch.arange(block, device=A.device)
+    i0, i1, i2 = torch.meshgrid(ar, ar, ar, indexing="ij")
+    rel = (i0 + grid * i1 + grid * grid * i2).permute(2, 1, 0).reshape(-1)  # local flat, axis 0 fastest
+    g = torch.arange(S, device=A.device)
+    base = block * (g % nb) + grid * block * ((g // nb) % nb) + grid * grid * block * (g // (nb * nb))
+    idx = (base[:, None] + rel[None, :]).reshape(-1)
+    G = torch.empty((n, grid ** 3), dtype=torch.float64, device=A.device)
+    G[:, idx] = A[:, :, qoi * b3:(qoi + 1) * b3].permute(1, 0, 2).reshape(n, -1)
+    return G.T  # m x n, column-major
+
+
+def archive_measure(cfg, A, args):
+    """the reference CLI's `compress --chunk 0` of a whole
+    structured field into the SPID archive container (spid_cli.cpp:195-232 +
+    archive.cpp encode) and its decompress, on the GPU through the C ABI.
+    Reference arm: the same CLI path compiled from the reference sources
+    (oracle/_ref), single-threaded as the CLI runs it, on a 64^3 sample whose
+    archive must be byte-identical to ours."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2103_01380_b200 import _native as N
+    from paper_2103_01380_b200 import archive as AR
+
+    grid, block, stride, k = cfg.grid, cfg.block, 2, cfg.k
+    field = global_field(A, grid, block, qoi=1)
+    m, n = field.shape
+    raw = m * n * 8
+    h = N.handle(torch.cuda.current_device())
+    rr = N.RankRule(N.RULE_FIXED, 0, k, 0, 0.0)
+    nb = C.c_int64()
+    out = {"workload": f"u of the {cfg.name} field: {grid}^3 x {n} fp64 ({raw / 1e9:.2f} GB), "
+                       f"{(grid // block) ** 3} blocks of {block}^3, stride {stride}, rank {k}"}
+
+    def compress(mode, src, on_dev):
+        spec = N.archive_spec((grid,) * 3, (grid // block,) * 3, (stride,) * 3, (1, 1, 1), mode,
+                              k + cfg.p, cfg.seed, "u", "bench")
+        h.check(N.lib.spidgpu_archive_compress(h.h, C.c_void_p(src), m, n, m, 1 if on_dev else 0,
+                                               C.byref(spec), C.byref(rr), C.byref(nb)))
+        return nb.value
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t) / reps
+
+    host = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
+    host.copy_(field.T)
+    for name, mode in (("sketch", N.ARCHIVE_SKETCH), ("exact", N.ARCHIVE_EXACT)):
+        s_dev = timed(lambda: compress(mode, field.data_ptr(), True), 3)
+        s_e2e = timed(lambda: compress(mode, host.data_ptr(), False), 2)
+        size = nb.value
+        view, ln = C.c_void_p(), C.c_int64()
+        h.check(N.lib.spidgpu_archive_view(h.h, C.byref(view), C.byref(ln)))
+        data = C.string_at(view.value, ln.value)
+        dec = torch.empty((n, m), dtype=torch.float64, device=field.device).T
+        s_dec = timed(lambda: AR.decompress(data, out=dec), 3)
+        err = float(torch.linalg.norm(dec - field) / torch.linalg.norm(field))
+        out[name] = {"archive_bytes": size, "cf": raw / size, "rel_frob_error": err,
+                     "device_ms": s_dev * 1e3, "device_gbs": raw / s_dev / 1e9,
+                     "e2e": {"value": raw / s_e2e / 1e9, "unit": "GB/s", "ms": s_e2e * 1e3,
+                             "h2d_bytes_per_step": raw, "d2h_bytes_per_step": size},
+                     "decompress_ms": s_dec * 1e3, "decompress_gbs": raw / s_dec / 1e9}
+        if name == "sketch":
+            out[name]["ell"] = k + cfg.p
+    del host
+    # reference CLI path on a 64^3 sub-field (8 blocks), byte parity with ours
+    try:
+        import oracle
+        ref = oracle.ref()
+        sg = 2 * block
+        sub = field.T.reshape(n, grid, grid, grid)[:, :sg, :sg, :sg]  # [n, z, y, x], x fastest
+        a_np = sub.reshape(n, -1).cpu().numpy().T  # m_sub x n, column-major
+        t = time.perf_counter()
+        rb = ref.compress_field(a_np, (sg,) * 3, (2, 2, 2), (stride,) * 3, rank=k, periodic=(0, 0, 0), qoi="u",
+                                provenance="bench")
+        t_ref = time.perf_counter() - t
+        t = time.perf_counter()
+        ref.archive_decompress(rb)
+        t_ref_dec = time.perf_counter() - t
+        ours = AR.compress_field(a_np, (sg,) * 3, (2, 2, 2), (stride,) * 3, rank=k, periodic=(0, 0, 0),
+                                 qoi="u", provenance="bench")
+        out["reference"] = {"kind": "reference", "cores": 1,
+                            "sample": f"{sg}^3 x {n} sub-field, 8 blocks (spid CLI batch path, oracle/_ref)",
+                            "compress_gbs": a_np.nbytes / t_ref / 1e9, "compress_s": t_ref,
+                            "decompress_gbs": a_np.nbytes / t_ref_dec / 1e9,
+                            "bytes_identical": ours == rb}
+    except Exception as e:  # reported, never fatal
+        out["reference"] = {"error": repr(e)}
+    return out
 
 
 def main():

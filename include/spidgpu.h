@@ -310,6 +310,9 @@ int spidgpu_archive_compress(spidgpu_handle h, const double* a, int64_t m, int64
                              int32_t a_on_device, const spidgpu_archive_spec* spec,
                              const spidgpu_rank_rule* rule, int64_t* nbytes);
 int spidgpu_archive_fetch(spidgpu_handle h, uint8_t* dst, int64_t cap);
+/* Zero-copy view of the same bytes (pinned host memory owned by the handle,
+ * valid until the next spidgpu_archive_compress or spidgpu_destroy). */
+int spidgpu_archive_view(spidgpu_handle h, const uint8_t** data, int64_t* nbytes);
 
 /* decode() header walk (archive.cpp:214-249) without the checksums: output
  * shape of decompress (rows = grid points, cols = snapshot count) and the

@@ -130,6 +130,7 @@ _SIGS = {
     "spidgpu_crc32": (C.c_int, [_H, _vp, _i64, C.c_int32, C.POINTER(C.c_uint32)]),
     "spidgpu_archive_compress": (C.c_int, [_H, _vp, _i64, _i64, _i64, C.c_int32, _AS, _RR, _pi64]),
     "spidgpu_archive_fetch": (C.c_int, [_H, _vp, _i64]),
+    "spidgpu_archive_view": (C.c_int, [_H, C.POINTER(_vp), _pi64]),
     "spidgpu_archive_shape": (C.c_int, [_vp, _i64, _pi64, _pi64, _pi64]),
     "spidgpu_archive_info": (C.c_int, [_H, _vp, _i64, _vp, _i64, _pi64]),
     "spidgpu_archive_decompress": (C.c_int, [_H, _vp, _i64, _vp, _i64, C.c_int32]),

@@ -32,7 +32,7 @@ def _is_cuda(a) -> bool:
 
 def compress_field(a, dims, blocks=None, strides=None, rank=None, tol=None, *, periodic=None,
                    qoi="", provenance="", mode=ARCHIVE_EXACT, ell=0, seed=0, rule: RankRule | None = None,
-                   device=0) -> bytes:
+                   out=None, device=0):
     """Batch SPID archive of a field: one spid() per block of
     make_block_domains(grid, blocks) with SubsampleSpec::strided(local,
     strides, include_boundary=True), then encode().
@@ -42,6 +42,9 @@ def compress_field(a, dims, blocks=None, strides=None, rank=None, tol=None, *, p
     column-major layout (a.T contiguous), used in place. mode=ARCHIVE_EXACT
     reproduces the reference's archive byte for byte; ARCHIVE_SKETCH puts an
     ell-row Gaussian sketch (Philox, `seed`) in front of each block's column ID.
+
+    Returns the archive as bytes, or -- when `out` (a uint8 buffer at least as
+    large as the archive) is given -- copies it there and returns its length.
     """
     nax = len(dims)
     blocks = list(blocks) if blocks is not None else [1] * nax
@@ -65,9 +68,14 @@ def compress_field(a, dims, blocks=None, strides=None, rank=None, tol=None, *, p
         rc = N.lib.spidgpu_archive_compress(h.h, C.c_void_p(af.ctypes.data), m, n, max(m, 1), 0,
                                             C.byref(spec), C.byref(rr.c()), C.byref(nbytes))
     h.check(rc)
-    out = np.empty(nbytes.value, dtype=np.uint8)
-    h.check(N.lib.spidgpu_archive_fetch(h.h, C.c_void_p(out.ctypes.data), nbytes.value))
-    return out.tobytes()
+    if out is not None:  # caller-owned buffer (numpy uint8 or pinned torch tensor)
+        ptr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
+        cap = out.numel() if hasattr(out, "numel") else out.size
+        h.check(N.lib.spidgpu_archive_fetch(h.h, C.c_void_p(ptr), cap))
+        return nbytes.value
+    view, n = C.c_void_p(), C.c_int64()
+    h.check(N.lib.spidgpu_archive_view(h.h, C.byref(view), C.byref(n)))
+    return C.string_at(view.value, n.value) if n.value else b""
 
 
 def _buf(data):

@@ -531,6 +531,7 @@ int spidgpu_destroy(spidgpu_handle h) {
     cudaSetDevice(h->device);
     cudaDeviceSynchronize();
     for (auto& w : h->ws) w.release();
+    if (h->archive_pinned) cudaFreeHost(h->archive_pinned);
     for (int i = 0; i < 2; ++i) {
         if (h->lanes[i]) cudaStreamDestroy(h->lanes[i]);
         if (h->ev[i]) cudaEventDestroy(h->ev[i]);

@@ -17,6 +17,8 @@
 //                       j-k-i order with its zero skip (dense_matrix.cpp:
 //                       38-53), rounded per operation -> bit-identical, written
 //                       straight into the assembled matrix (blocking.cpp:219-241).
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -167,13 +169,8 @@ __device__ uint32_t crc_raw_range(const uint8_t* __restrict__ data, int64_t lo, 
 
 constexpr int kCrcThreads = 256;
 
-// One CTA per section: 256 contiguous end-aligned chunks, slice-by-8 each,
-// combined through x^(8*len) shifts (crc.cu explains the identities).
-__global__ void __launch_bounds__(kCrcThreads)
-    crc_sections_kernel(const uint8_t* __restrict__ data, const CrcSection* __restrict__ secs,
-                        int64_t nsec, uint32_t* __restrict__ crc_out, uint8_t* write_back) {
-    __shared__ uint32_t T[8][256];
-    __shared__ uint32_t part[kCrcThreads / kWarp];
+// CRC tables (slice-by-8) built once per CTA in shared memory.
+__device__ void build_crc_tables(uint32_t (*T)[256]) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) {
         uint32_t c = i;
         for (int b = 0; b < 8; ++b) c = (c & 1) ? (c >> 1) ^ kPolyR : c >> 1;
@@ -185,15 +182,27 @@ __global__ void __launch_bounds__(kCrcThreads)
             T[t][i] = (T[t - 1][i] >> 8) ^ T[0][T[t - 1][i] & 0xff];
         __syncthreads();
     }
+}
+
+// Raw CRC of each part (<= kCrcPart bytes, end-aligned inside its section):
+// 256 contiguous end-aligned chunks per part, combined through x^(8*len)
+// shifts (crc.cu explains the identities).
+__global__ void __launch_bounds__(kCrcThreads)
+    crc_parts_kernel(const uint8_t* __restrict__ data, const CrcPart* __restrict__ parts,
+                     int64_t nparts, uint32_t* __restrict__ part_crc) {
+    __shared__ uint32_t T[8][256];
+    __shared__ uint32_t part[kCrcThreads / kWarp];
+    build_crc_tables(T);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int64_t s = blockIdx.x; s < nsec; s += gridDim.x) {
-        const int64_t begin = secs[s].begin, len = secs[s].len, end = begin + len;
-        const int64_t C = len > 0 ? (len + kCrcThreads - 1) / kCrcThreads : 1;
+    constexpr int64_t C = kCrcPart / kCrcThreads;
+    uint32_t X0 = xpow8_d(static_cast<uint64_t>(C));
+    for (int64_t q = blockIdx.x; q < nparts; q += gridDim.x) {
+        const int64_t begin = parts[q].begin, end = parts[q].end;
         int64_t lo = end - (kCrcThreads - threadIdx.x) * C;
         const int64_t hi = lo + C;
         if (lo < begin) lo = begin;
         uint32_t c = lo < hi ? crc_raw_range(data, lo, hi, T) : 0u;
-        uint32_t X = xpow8_d(static_cast<uint64_t>(C));  // shift past one chunk
+        uint32_t X = X0;
 #pragma unroll
         for (int j = 0; j < 5; ++j) {
             const uint32_t other = __shfl_down_sync(0xffffffffu, c, 1 << j);
@@ -205,14 +214,29 @@ __global__ void __launch_bounds__(kCrcThreads)
         if (threadIdx.x == 0) {
             uint32_t acc = part[0];
             for (int w = 1; w < kCrcThreads / kWarp; ++w) acc = multmodp_d(X, acc) ^ part[w];
-            const uint32_t crc = ~(acc ^ multmodp_d(xpow8_d(static_cast<uint64_t>(len)), 0xFFFFFFFFu));
-            crc_out[s] = crc;
-            if (write_back) {
-#pragma unroll
-                for (int b = 0; b < 4; ++b) write_back[end + b] = static_cast<uint8_t>(crc >> (8 * b));
-            }
+            part_crc[q] = acc;
         }
         __syncthreads();
+    }
+}
+
+// One thread per section: fold its parts (all but the first are kCrcPart
+// long), condition, optionally write the 4 CRC bytes after the payload.
+__global__ void crc_fold_kernel(const CrcSection* __restrict__ secs, int64_t nsec,
+                                const int64_t* __restrict__ first_part, const uint32_t* __restrict__ part_crc,
+                                uint32_t* __restrict__ crc_out, uint8_t* write_back) {
+    const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (s >= nsec) return;
+    const uint32_t xpart = xpow8_d(static_cast<uint64_t>(kCrcPart));
+    uint32_t acc = 0;
+    for (int64_t q = first_part[s]; q < first_part[s + 1]; ++q) acc = multmodp_d(xpart, acc) ^ part_crc[q];
+    const int64_t len = secs[s].len;
+    const uint32_t crc = ~(acc ^ multmodp_d(xpow8_d(static_cast<uint64_t>(len)), 0xFFFFFFFFu));
+    crc_out[s] = crc;
+    if (write_back) {
+        const int64_t end = secs[s].begin + len;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) write_back[end + b] = static_cast<uint8_t>(crc >> (8 * b));
     }
 }
 
@@ -284,24 +308,57 @@ __global__ void __launch_bounds__(kReconRows)
     }
 }
 
+__device__ __forceinline__ bool nonfinite_bits(double v) {
+    return (__double_as_longlong(v) & 0x7ff0000000000000LL) == 0x7ff0000000000000LL;
+}
+
+// blockIdx.y walks columns, threads walk rows: no per-element index division;
+// the block of a non-finite entry is located only on a hit.
+__device__ __noinline__ void flag_block(int64_t r, const BlockGridDev& g, int32_t* flags) {
+    int64_t rem = r, blk = 0, mul = 1;
+    for (int ax = 0; ax < g.naxes; ++ax) {
+        const int64_t coord = rem % g.dims[ax];
+        rem /= g.dims[ax];
+        int64_t seg = coord / g.seg_base[ax];
+        if (seg >= g.seg_count[ax]) seg = g.seg_count[ax] - 1;
+        blk += seg * mul;
+        mul *= g.seg_count[ax];
+    }
+    atomicExch(flags + blk, 1);
+}
+
+// kVec: 16-byte loads, four in flight per thread (lda even, A 16-byte aligned).
+template <bool kVec>
 __global__ void nonfinite_blocks_kernel(const double* __restrict__ A, int64_t lda, int64_t m,
                                         int64_t n, BlockGridDev g, int32_t* __restrict__ flags) {
-    const int64_t total = m * n;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t r = e % m, j = e / m;
-        const double v = A[j * lda + r];
-        if (isfinite(v)) continue;
-        int64_t rem = r, blk = 0, mul = 1;
-        for (int ax = 0; ax < g.naxes; ++ax) {
-            const int64_t coord = rem % g.dims[ax];
-            rem /= g.dims[ax];
-            int64_t seg = coord / g.seg_base[ax];
-            if (seg >= g.seg_count[ax]) seg = g.seg_count[ax] - 1;
-            blk += seg * mul;
-            mul *= g.seg_count[ax];
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    for (int64_t j = blockIdx.y; j < n; j += gridDim.y) {
+        const double* col = A + j * lda;
+        if (kVec) {
+            const double2* c2 = reinterpret_cast<const double2*>(col);
+            const int64_t m2 = m / 2;
+            int64_t r = t0;
+            for (; r + 3 * stride < m2; r += 4 * stride) {
+                double2 v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = __ldcs(c2 + r + u * stride);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (nonfinite_bits(v[u].x)) flag_block(2 * (r + u * stride), g, flags);
+                    if (nonfinite_bits(v[u].y)) flag_block(2 * (r + u * stride) + 1, g, flags);
+                }
+            }
+            for (; r < m2; r += stride) {
+                const double2 v = __ldcs(c2 + r);
+                if (nonfinite_bits(v.x)) flag_block(2 * r, g, flags);
+                if (nonfinite_bits(v.y)) flag_block(2 * r + 1, g, flags);
+            }
+            if ((m & 1) && t0 == 0 && nonfinite_bits(col[m - 1])) flag_block(m - 1, g, flags);
+        } else {
+            for (int64_t r = t0; r < m; r += stride)
+                if (nonfinite_bits(__ldcs(col + r))) flag_block(r, g, flags);
         }
-        if (rem == 0) atomicExch(flags + blk, 1);  // rows past the grid are ignored
     }
 }
 
@@ -338,11 +395,32 @@ cudaError_t launch_pack_blocks(const PackBlock* blocks, int64_t nblocks, int64_t
     return cudaGetLastError();
 }
 
+void crc_plan_parts(const CrcSection* secs, int64_t nsec, std::vector<CrcPart>* parts,
+                    std::vector<int64_t>* first_part) {
+    parts->clear();
+    first_part->assign(1, 0);
+    for (int64_t s = 0; s < nsec; ++s) {
+        const int64_t b = secs[s].begin, e = b + secs[s].len;
+        const int64_t np = secs[s].len > 0 ? (secs[s].len + kCrcPart - 1) / kCrcPart : 1;
+        for (int64_t q = 0; q < np; ++q) {
+            const int64_t hi = e - (np - 1 - q) * kCrcPart;
+            parts->push_back({hi - kCrcPart > b ? hi - kCrcPart : b, hi});
+        }
+        first_part->push_back(static_cast<int64_t>(parts->size()));
+    }
+}
+
 cudaError_t launch_crc_sections(const uint8_t* data, const CrcSection* secs, int64_t nsec,
-                                uint32_t* crc_out, uint8_t* write_back, cudaStream_t st) {
-    const int64_t g = nsec < 148 * 8 ? nsec : 148 * 8;
-    crc_sections_kernel<<<static_cast<unsigned>(g < 1 ? 1 : g), kCrcThreads, 0, st>>>(
-        data, secs, nsec, crc_out, write_back);
+                                const CrcPart* parts, int64_t nparts, const int64_t* first_part,
+                                uint32_t* part_crc, uint32_t* crc_out, uint8_t* write_back,
+                                cudaStream_t st) {
+    const int64_t g = nparts < 148 * 8 ? nparts : 148 * 8;
+    crc_parts_kernel<<<static_cast<unsigned>(g < 1 ? 1 : g), kCrcThreads, 0, st>>>(data, parts, nparts,
+                                                                                 part_crc);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    crc_fold_kernel<<<static_cast<unsigned>((nsec + 127) / 128), 128, 0, st>>>(secs, nsec, first_part, part_crc,
+                                                                               crc_out, write_back);
     return cudaGetLastError();
 }
 
@@ -375,7 +453,17 @@ cudaError_t launch_recon_scatter(const double* F, int64_t ldf, int64_t strideF, 
 
 cudaError_t launch_nonfinite_blocks(const double* A, int64_t lda, int64_t m, int64_t n,
                                     const BlockGridDev& g, int32_t* flags, cudaStream_t st) {
-    nonfinite_blocks_kernel<<<grid_for(m * n, 256), 256, 0, st>>>(A, lda, m, n, g, flags);
+    // ~8 resident CTAs per SM in total, rows split so each thread streams >= 8 entries
+    int64_t gy = n < 65535 ? n : 65535;
+    int64_t gx = (148 * 8 + gy - 1) / gy;
+    const int64_t gx_max = (m + 256 * 8 - 1) / (256 * 8);
+    if (gx > gx_max) gx = gx_max;
+    if (gx < 1) gx = 1;
+    const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy));
+    if (lda % 2 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0)
+        nonfinite_blocks_kernel<true><<<grid, 256, 0, st>>>(A, lda, m, n, g, flags);
+    else
+        nonfinite_blocks_kernel<false><<<grid, 256, 0, st>>>(A, lda, m, n, g, flags);
     return cudaGetLastError();
 }
 

@@ -5,6 +5,8 @@
 // sequences launches; gathers, column IDs, packing, checksums, unpacking,
 // lifting and the reconstruct/assemble run in the kernels of archive.cu,
 // cpqr*.cu, sketch.cu, gather.cu and interp.cu.
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -159,6 +161,33 @@ struct Carve {
         const size_t o = off;
         off += sizeof(T) * std::max<size_t>(count, 1);
         return o;
+    }
+};
+
+// SPIDGPU_TRACE=1: per-phase device times of the archive calls on stderr.
+struct Trace {
+    bool on = std::getenv("SPIDGPU_TRACE") != nullptr;
+    cudaStream_t st;
+    std::vector<std::pair<std::string, cudaEvent_t>> marks;
+    explicit Trace(cudaStream_t s) : st(s) { mark("start"); }
+    void mark(const char* name) {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        marks.emplace_back(name, e);
+    }
+    ~Trace() {
+        if (!on) return;
+        cudaEventSynchronize(marks.back().second);
+        std::string line = "[spidgpu trace]";
+        for (size_t i = 1; i < marks.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
+            line += " " + marks[i].first + "=" + std::to_string(ms) + "ms";
+        }
+        std::fprintf(stderr, "%s\n", line.c_str());
+        for (auto& m : marks) cudaEventDestroy(m.second);
     }
 };
 
@@ -348,20 +377,32 @@ int decode_archive(spidgpu_handle h, const uint8_t* bytes, int64_t nbytes, Decod
     frame_archive(bytes, nbytes, &F);
     if (F.secs.empty()) return fail(h, F.status, F.msg);
     Workspace& ws = h->ws[0];
-    Carve cv;
-    const size_t o_bytes = cv.take<uint8_t>(static_cast<size_t>(nbytes));
-    const size_t o_secs = cv.take<CrcSection>(F.secs.size());
-    const size_t o_crc = cv.take<uint32_t>(F.secs.size());
-    CK(h, ws.bytes.ensure(cv.off, st));
     std::vector<CrcSection> secs;
     for (const SecRef& s : F.secs) secs.push_back({s.begin, s.len});
+    std::vector<CrcPart> parts;
+    std::vector<int64_t> first_part;
+    crc_plan_parts(secs.data(), static_cast<int64_t>(secs.size()), &parts, &first_part);
+    Carve cv;
+    const size_t o_bytes = cv.take<uint8_t>(static_cast<size_t>(nbytes));
+    const size_t o_secs = cv.take<CrcSection>(secs.size());
+    const size_t o_crc = cv.take<uint32_t>(secs.size());
+    const size_t o_parts = cv.take<CrcPart>(parts.size());
+    const size_t o_first = cv.take<int64_t>(first_part.size());
+    const size_t o_pcrc = cv.take<uint32_t>(parts.size());
+    CK(h, ws.bytes.ensure(cv.off, st));
     CK(h, cudaMemcpyAsync(at<uint8_t>(ws.bytes, o_bytes), bytes, static_cast<size_t>(nbytes),
                           cudaMemcpyHostToDevice, st));
     CK(h, cudaMemcpyAsync(at<CrcSection>(ws.bytes, o_secs), secs.data(),
                           sizeof(CrcSection) * secs.size(), cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(at<CrcPart>(ws.bytes, o_parts), parts.data(), sizeof(CrcPart) * parts.size(),
+                          cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(at<int64_t>(ws.bytes, o_first), first_part.data(),
+                          sizeof(int64_t) * first_part.size(), cudaMemcpyHostToDevice, st));
     CK(h, launch_crc_sections(at<uint8_t>(ws.bytes, o_bytes), at<CrcSection>(ws.bytes, o_secs),
-                              static_cast<int64_t>(secs.size()), at<uint32_t>(ws.bytes, o_crc), nullptr, st));
-    h->launches += 1;
+                              static_cast<int64_t>(secs.size()), at<CrcPart>(ws.bytes, o_parts),
+                              static_cast<int64_t>(parts.size()), at<int64_t>(ws.bytes, o_first),
+                              at<uint32_t>(ws.bytes, o_pcrc), at<uint32_t>(ws.bytes, o_crc), nullptr, st));
+    h->launches += 2;
     std::vector<uint32_t> crcs(secs.size());
     CK(h, cudaMemcpyAsync(crcs.data(), at<uint32_t>(ws.bytes, o_crc), sizeof(uint32_t) * crcs.size(),
                           cudaMemcpyDeviceToHost, st));
@@ -499,6 +540,7 @@ int spidgpu_archive_compress(spidgpu_handle h, const double* a, int64_t m, int64
     const size_t o_secs = cv.take<CrcSection>(nblocks + 1);
     const size_t o_crc = cv.take<uint32_t>(nblocks + 1);
     CK(h, ws.bsk.ensure(cv.off, st));
+    Trace tr(st);
 
     const double* A = a;
     int64_t ldA = lda;
@@ -519,6 +561,7 @@ int spidgpu_archive_compress(spidgpu_handle h, const double* a, int64_t m, int64
     CK(h, cudaMemsetAsync(at<int32_t>(ws.bsk, o_flags), 0, sizeof(int32_t) * nblocks, st));
     CK(h, launch_nonfinite_blocks(A, ldA, L.points, n, bg, at<int32_t>(ws.bsk, o_flags), st));
     h->launches += 1;
+    tr.mark("h2d+scan");
 
     spidgpu_rank_rule r = *rule;
     for (size_t gi = 0; gi < groups.size(); ++gi) {
@@ -534,6 +577,7 @@ int spidgpu_archive_compress(spidgpu_handle h, const double* a, int64_t m, int64
         CK(h, launch_gather_block_rows(A, ldA, at<int64_t>(ws.bsk, p.o_rel), p.Pc,
                                        at<int64_t>(ws.bsk, p.o_bases), p.nb, n, B, p.ldb, p.ldb * n, st));
         h->launches += 1;
+        tr.mark("gather");
         const double* Ycp = B;
         int64_t ldy = p.ldb, rows = p.Pc;
         if (sketch) {
@@ -548,6 +592,7 @@ int spidgpu_archive_compress(spidgpu_handle h, const double* a, int64_t m, int64
             Ycp = Y;
             ldy = spec->ell;
             rows = spec->ell;
+            tr.mark("sketch");
         }
         CK(h, cudaMemsetAsync(at<double>(ws.bsk, p.o_C), 0, sizeof(double) * p.nb * p.kcap * n, st));
         rc = do_cpqr(h, ws, Ycp, rows, n, ldy, ldy * n, p.nb, &r, p.kcap, at<int64_t>(ws.bsk, p.o_idx),
@@ -555,6 +600,7 @@ int spidgpu_archive_compress(spidgpu_handle h, const double* a, int64_t m, int64
                      at<double>(ws.bsk, p.o_resid), at<int32_t>(ws.bsk, p.o_status), nullptr, nullptr,
                      nullptr, st);
         if (rc) return rc;
+        tr.mark("cpqr");
         // f.base.skeleton = B(:, I) (id.cpp:82): coarse rows of the block
         rc = do_gather(h, B, p.Pc, n, p.ldb, p.ldb * n, p.nb, at<int64_t>(ws.bsk, p.o_idx), p.kcap,
                        at<int64_t>(ws.bsk, p.o_rank), at<double>(ws.bsk, p.o_skel), p.Pc, p.Pc * p.kcap, st);
@@ -562,6 +608,7 @@ int spidgpu_archive_compress(spidgpu_handle h, const double* a, int64_t m, int64
         CK(h, launch_sort_union(at<int64_t>(ws.bsk, p.o_idx), p.kcap, at<int64_t>(ws.bsk, p.o_rank), p.nb,
                                 at<int64_t>(ws.bsk, p.o_uni), st));
         h->launches += 1;
+        tr.mark("skel+sort");
     }
     // per-block ranks / statuses back to the host (one small copy per group)
     std::vector<int32_t> flags(nblocks);
@@ -648,6 +695,14 @@ int spidgpu_archive_compress(spidgpu_handle h, const double* a, int64_t m, int64
         off += 8 + payload + 4;
     }
     const int64_t total = off;
+    std::vector<CrcPart> parts;
+    std::vector<int64_t> first_part;
+    crc_plan_parts(secs.data(), static_cast<int64_t>(secs.size()), &parts, &first_part);
+    Carve cc;
+    const size_t o_parts = cc.take<CrcPart>(parts.size());
+    const size_t o_first = cc.take<int64_t>(first_part.size());
+    const size_t o_pcrc = cc.take<uint32_t>(parts.size());
+    CK(h, ws.crc.ensure(cc.off, st));
     CK(h, ws.bytes.ensure(static_cast<size_t>(total), st));
     uint8_t* dev = ws.bytes.as<uint8_t>();
     CK(h, cudaMemcpyAsync(dev, head.data(), head.size(), cudaMemcpyHostToDevice, st));
@@ -655,22 +710,50 @@ int spidgpu_archive_compress(spidgpu_handle h, const double* a, int64_t m, int64
                           cudaMemcpyHostToDevice, st));
     CK(h, cudaMemcpyAsync(at<CrcSection>(ws.bsk, o_secs), secs.data(), sizeof(CrcSection) * secs.size(),
                           cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(at<CrcPart>(ws.crc, o_parts), parts.data(), sizeof(CrcPart) * parts.size(),
+                          cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(at<int64_t>(ws.crc, o_first), first_part.data(), sizeof(int64_t) * first_part.size(),
+                          cudaMemcpyHostToDevice, st));
+    tr.mark("host-layout");
     CK(h, launch_pack_blocks(at<PackBlock>(ws.bsk, o_pack), nblocks, max_items, dev, st));
-    CK(h, launch_crc_sections(dev, at<CrcSection>(ws.bsk, o_secs), nblocks + 1,
-                              at<uint32_t>(ws.bsk, o_crc), dev, st));
-    h->launches += 2;
-    h->archive.resize(static_cast<size_t>(total));
-    CK(h, cudaMemcpyAsync(h->archive.data(), dev, static_cast<size_t>(total), cudaMemcpyDeviceToHost, st));
+    tr.mark("pack");
+    CK(h, launch_crc_sections(dev, at<CrcSection>(ws.bsk, o_secs), nblocks + 1, at<CrcPart>(ws.crc, o_parts),
+                              static_cast<int64_t>(parts.size()), at<int64_t>(ws.crc, o_first),
+                              at<uint32_t>(ws.crc, o_pcrc), at<uint32_t>(ws.bsk, o_crc), dev, st));
+    h->launches += 3;
+    tr.mark("crc");
+    // one device-to-host copy of the finished archive into pinned memory
+    if (h->archive_cap < static_cast<size_t>(total)) {
+        CK(h, cudaStreamSynchronize(st));
+        const size_t want = std::max(static_cast<size_t>(total), h->archive_cap * 3 / 2);
+        if (h->archive_pinned) cudaFreeHost(h->archive_pinned);
+        h->archive_pinned = nullptr;
+        h->archive_cap = 0;
+        h->archive_size = 0;
+        CK(h, cudaHostAlloc(reinterpret_cast<void**>(&h->archive_pinned), want, cudaHostAllocDefault));
+        h->archive_cap = want;
+    }
+    CK(h, cudaMemcpyAsync(h->archive_pinned, dev, static_cast<size_t>(total), cudaMemcpyDeviceToHost, st));
+    tr.mark("d2h");
     CK(h, cudaStreamSynchronize(st));
+    h->archive_size = static_cast<size_t>(total);
     *nbytes = total;
     return SPID_OK;
 }
 
 int spidgpu_archive_fetch(spidgpu_handle h, uint8_t* dst, int64_t cap) {
     if (!h) return SPID_INVALID_ARGUMENT;
-    if (!dst || cap < static_cast<int64_t>(h->archive.size()))
+    if (!dst || cap < static_cast<int64_t>(h->archive_size))
         return fail(h, SPID_INVALID_ARGUMENT, "destination smaller than the archive");
-    std::memcpy(dst, h->archive.data(), h->archive.size());
+    if (h->archive_size) std::memcpy(dst, h->archive_pinned, h->archive_size);
+    return SPID_OK;
+}
+
+int spidgpu_archive_view(spidgpu_handle h, const uint8_t** data, int64_t* nbytes) {
+    if (!h) return SPID_INVALID_ARGUMENT;
+    if (!data || !nbytes) return fail(h, SPID_INVALID_ARGUMENT, "null output");
+    *data = h->archive_pinned;
+    *nbytes = static_cast<int64_t>(h->archive_size);
     return SPID_OK;
 }
 
@@ -735,7 +818,9 @@ int spidgpu_archive_decompress(spidgpu_handle h, const uint8_t* bytes, int64_t n
     Workspace& ws = h->ws[0];
     cudaStream_t st = h->lanes[0];
     Decoded D;
+    Trace tr(st);
     int rc = decode_archive(h, bytes, nbytes, &D, st);  // leaves the archive bytes in ws.bytes
+    tr.mark("h2d+crc");
     if (rc) return rc;
     const uint8_t* dev_bytes = ws.bytes.as<uint8_t>();
     Layout L;
@@ -857,6 +942,7 @@ int spidgpu_archive_decompress(spidgpu_handle h, const uint8_t* bytes, int64_t n
         CK(h, cudaMemcpyAsync(at<UnpackBlock>(ws.bsk, p.o_unpack), ub.data(), sizeof(UnpackBlock) * p.nb,
                               cudaMemcpyHostToDevice, st));
         CK(h, launch_unpack_blocks(dev_bytes, at<UnpackBlock>(ws.bsk, p.o_unpack), p.nb, max_items, st));
+        tr.mark("unpack");
         h->launches += 1;
         const double* Fm = at<double>(ws.bsk, p.o_S);
         if (G.coarse) {  // lift.apply(skeleton) (interp.cpp:168-186)
@@ -865,12 +951,14 @@ int spidgpu_archive_decompress(spidgpu_handle h, const uint8_t* bytes, int64_t n
                                       p.mb * p.kcap, nullptr, st));
             h->launches += 1;
             Fm = at<double>(ws.bsk, p.o_F);
+            tr.mark("lift");
         }
         CK(h, launch_recon_scatter(Fm, p.mb, p.mb * p.kcap, at<double>(ws.bsk, p.o_C), p.kcap,
                                    p.kcap * ncols, at<int64_t>(ws.bsk, p.o_rank), p.nb, p.mb, ncols,
                                    at<int64_t>(ws.bsk, p.o_rel), at<int64_t>(ws.bsk, p.o_bases), outd, ldd,
                                    st));
         h->launches += 1;
+        tr.mark("recon");
     }
     if (!out_on_device)
         CK(h, cudaMemcpy2DAsync(out, sizeof(double) * ldo, outd, sizeof(double) * mout, sizeof(double) * mout,

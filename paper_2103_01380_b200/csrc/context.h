@@ -81,7 +81,8 @@ struct spidgpu_context {
     int64_t launches = 0;
     std::string last_error;
     bool force_generic_cpqr = false;  // tests: exercise the shared/global-W kernel too
-    std::vector<uint8_t> archive;     // last archive built by spidgpu_archive_compress
+    uint8_t* archive_pinned = nullptr;  // last archive built by spidgpu_archive_compress
+    size_t archive_cap = 0, archive_size = 0;
 };
 
 namespace spidgpu {

@@ -32,6 +32,15 @@ constexpr int kCpqrThreads = 256;
 constexpr double kZeroFloor = 1e-300;  // qr.cpp:11
 constexpr double kCollapseRel = 1e-14; // qr.cpp:12
 
+constexpr int kPf = 32;  // rows per prefetched chunk of the column sweeps
+
+// wv[u] = W[(i0 + u) * npad + col] for rows < `rows` (0 past the end).
+__device__ __forceinline__ void load_chunk(const double* W, int npad, int col, int i0, int rows,
+                                           double (&wv)[kPf]) {
+#pragma unroll
+    for (int u = 0; u < kPf; ++u) wv[u] = i0 + u < rows ? W[(i0 + u) * npad + col] : 0.0;
+}
+
 struct CpqrShared {
     double best_v;
     int best_i;
@@ -124,10 +133,12 @@ __global__ void __launch_bounds__(kCpqrThreads)
     double lmax = 0.0;
     for (int j = tid; j < n; j += kCpqrThreads) {
         double s = 0.0;
-#pragma unroll 8
-        for (int i = 0; i < rows; ++i) {
-            const double w = W[i * npad + j];
-            s = add_rn(s, mul_rn(w, w));
+        for (int i0 = 0; i0 < rows; i0 += kPf) {
+            double wv[kPf];
+            load_chunk(W, npad, j, i0, rows, wv);
+#pragma unroll
+            for (int u = 0; u < kPf; ++u)
+                if (i0 + u < rows) s = add_rn(s, mul_rn(wv[u], wv[u]));
         }
         const double v = sqrt(s);
         nrm[j] = v;
@@ -225,23 +236,45 @@ __global__ void __launch_bounds__(kCpqrThreads)
         // next step's fresh norm (qr.cpp:66-67) is accumulated in pass 2.
         for (int j = tid; j < n; j += kCpqrThreads) {
             if (posof[j] <= s) continue;
+            // rows are consumed in chunks whose loads are all issued before the
+            // chunk's (sequential, separately rounded) arithmetic: the sums keep
+            // the reference's order, the memory latency is paid once per chunk
             double r1 = 0.0;
-#pragma unroll 8
-            for (int i = 0; i < rows; ++i) r1 = add_rn(r1, mul_rn(W[i * npad + pc], W[i * npad + j]));
+            for (int i0 = 0; i0 < rows; i0 += kPf) {
+                double qv[kPf], wv[kPf];
+                load_chunk(W, npad, pc, i0, rows, qv);
+                load_chunk(W, npad, j, i0, rows, wv);
+#pragma unroll
+                for (int u = 0; u < kPf; ++u)
+                    if (i0 + u < rows) r1 = add_rn(r1, mul_rn(qv[u], wv[u]));
+            }
             double r2 = 0.0;
-#pragma unroll 8
-            for (int i = 0; i < rows; ++i) {
-                const double q = W[i * npad + pc];
-                const double w = sub_rn(W[i * npad + j], mul_rn(r1, q));
-                W[i * npad + j] = w;
-                r2 = add_rn(r2, mul_rn(q, w));
+            for (int i0 = 0; i0 < rows; i0 += kPf) {
+                double qv[kPf], wv[kPf];
+                load_chunk(W, npad, pc, i0, rows, qv);
+                load_chunk(W, npad, j, i0, rows, wv);
+#pragma unroll
+                for (int u = 0; u < kPf; ++u) {
+                    if (i0 + u < rows) {
+                        const double w = sub_rn(wv[u], mul_rn(r1, qv[u]));
+                        W[(i0 + u) * npad + j] = w;
+                        r2 = add_rn(r2, mul_rn(qv[u], w));
+                    }
+                }
             }
             double nn = 0.0;
-#pragma unroll 8
-            for (int i = 0; i < rows; ++i) {
-                const double w = sub_rn(W[i * npad + j], mul_rn(r2, W[i * npad + pc]));
-                W[i * npad + j] = w;
-                nn = add_rn(nn, mul_rn(w, w));
+            for (int i0 = 0; i0 < rows; i0 += kPf) {
+                double qv[kPf], wv[kPf];
+                load_chunk(W, npad, pc, i0, rows, qv);
+                load_chunk(W, npad, j, i0, rows, wv);
+#pragma unroll
+                for (int u = 0; u < kPf; ++u) {
+                    if (i0 + u < rows) {
+                        const double w = sub_rn(wv[u], mul_rn(r2, qv[u]));
+                        W[(i0 + u) * npad + j] = w;
+                        nn = add_rn(nn, mul_rn(w, w));
+                    }
+                }
             }
             R[static_cast<size_t>(s) * n + j] = add_rn(r1, r2);
             nrm[j] = sqrt(nn);

@@ -6,6 +6,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <vector>
+
 namespace spidgpu {
 
 enum RuleMode { RULE_FIXED = 0, RULE_TOL = 1, RULE_BLOCKED = 2 };
@@ -158,6 +160,10 @@ struct PackBlock {          // one block section of the archive
 struct CrcSection {
     int64_t begin, len;     // payload byte range; the CRC follows it
 };
+constexpr int64_t kCrcPart = 65536;  // bytes per CTA work unit of the section CRC
+struct CrcPart {
+    int64_t begin, end;     // <= kCrcPart bytes, end-aligned inside a section
+};
 struct UnpackBlock {
     int64_t skel_off, coef_off;  // archive offsets of the first f64 of each matrix
     int64_t mc, k, n;
@@ -177,8 +183,13 @@ cudaError_t launch_sort_union(const int64_t* idx, int64_t kcap, const int64_t* r
                               int64_t* uni, cudaStream_t st);
 cudaError_t launch_pack_blocks(const PackBlock* blocks, int64_t nblocks, int64_t max_items,
                                uint8_t* out, cudaStream_t st);
+// host: split sections into parts (first_part has nsec + 1 entries)
+void crc_plan_parts(const CrcSection* secs, int64_t nsec, std::vector<CrcPart>* parts,
+                    std::vector<int64_t>* first_part);
 cudaError_t launch_crc_sections(const uint8_t* data, const CrcSection* secs, int64_t nsec,
-                                uint32_t* crc_out, uint8_t* write_back, cudaStream_t st);
+                                const CrcPart* parts, int64_t nparts, const int64_t* first_part,
+                                uint32_t* part_crc, uint32_t* crc_out, uint8_t* write_back,
+                                cudaStream_t st);
 cudaError_t launch_unpack_blocks(const uint8_t* bytes, const UnpackBlock* blocks, int64_t nblocks,
                                  int64_t max_items, cudaStream_t st);
 cudaError_t launch_recon_scatter(const double* F, int64_t ldf, int64_t strideF, const double* C,
