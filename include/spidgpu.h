@@ -334,6 +334,66 @@ int spidgpu_archive_decompress(spidgpu_handle h, const uint8_t* bytes, int64_t n
                                int64_t ldo, int32_t out_on_device);
 
 /* =====================================================================
+ * Streaming two-stage compressor -- SURVEY 8(f)2. Replaces run_pipeline
+ * (proj/src/pipeline.cpp:104-294, proj/include/spid/pipeline.hpp): snapshots
+ * are pushed as they are produced; every block's coarse rows are buffered in
+ * device memory into temporal chunks of time_chunk columns; each closed chunk
+ * runs stage 1 (column_id_at_most(chunk, min(k, cols)), blocking.cpp:112-115)
+ * for all blocks at once on a second CUDA stream while ingestion continues
+ * (at most 2 chunks in flight per block, the reference's backpressure);
+ * finish runs stage 2 (stage2_compress, blocking.cpp:128-204: tolerance ID of
+ * the union of stage-1 skeletons, composed coefficients) for all blocks and
+ * emits the "two-stage" archive. The archive is byte-identical to
+ * encode(run_pipeline(...).archive) for the same snapshots.
+ * ===================================================================== */
+typedef struct spidgpu_stream_config {
+    int32_t naxes;              /* structured grid, 1..3 axes                   */
+    int32_t include_boundary;   /* StreamConfig::include_boundary               */
+    int64_t dims[3];
+    int32_t periodic[3];
+    int32_t reserved;
+    int64_t blocks_per_axis[3]; /* PartitionPlan::blocks_per_axis               */
+    int64_t strides[3];         /* StreamConfig::strides                        */
+    int64_t time_chunk;         /* PartitionPlan::time_chunk (>= 1)             */
+    int64_t stage1_rank;        /* StreamConfig::stage1_rank (>= 1)             */
+    double stage2_tol;          /* StreamConfig::stage2_tol                     */
+    const char* qoi;
+    const char* provenance;
+} spidgpu_stream_config;
+
+typedef struct spidgpu_stream_stats {
+    int64_t snapshots;           /* frames ingested                             */
+    int64_t stage1_tasks;        /* (block, chunk) stage-1 IDs run              */
+    int64_t stage2_tasks;        /* blocks merged by stage 2                    */
+    int64_t fine_entries_peak;   /* device frame staging (entries)              */
+    int64_t coarse_entries_peak; /* chunk buffers (entries), cf. BufferStats    */
+    double stage1_ms;            /* device time of all stage-1 launches         */
+    double stage2_ms;            /* device time of stage 2 + archive emission   */
+} spidgpu_stream_stats;
+
+typedef struct spidgpu_stream* spidgpu_stream_handle;
+
+/* Validates the plan (UnstructuredNoInterp, BadStreamConfig, BlockTooSmall,
+ * BadSubsampleSpec as run_pipeline does before ingesting). The stream owns
+ * its CUDA streams and buffers; `h` receives the archive at finish. */
+int spidgpu_stream_open(spidgpu_handle h, const spidgpu_stream_config* cfg,
+                        spidgpu_stream_handle* out);
+/* Push `count` snapshots (m x count, ld ld; m must equal the grid's point
+ * count, else GeometryMismatch). on_device != 0: `frames` is a device pointer
+ * that may be reused when the call returns. */
+int spidgpu_stream_push(spidgpu_stream_handle s, const double* frames, int64_t m, int64_t count,
+                        int64_t ld, int32_t on_device);
+/* Close the final short chunks, run stage 2, emit the archive into the parent
+ * handle (spidgpu_archive_view / spidgpu_archive_fetch). Stage-1 failures are
+ * reported here, naming the first failing block and chunk; ShortStream when
+ * nothing was pushed. */
+int spidgpu_stream_finish(spidgpu_stream_handle s, int64_t* nbytes);
+int spidgpu_stream_get_stats(spidgpu_stream_handle s, spidgpu_stream_stats* out);
+/* Message of the stream's last failure ("" if none). */
+const char* spidgpu_stream_last_error(spidgpu_stream_handle s);
+int spidgpu_stream_close(spidgpu_stream_handle s);
+
+/* =====================================================================
  * Synthetic input fields (bench/tests only; not a reference interface).
  * Taylor-Green-vortex families of BASELINE.json configs 1-5, generated in
  * place on the device for a batch of subdomains of a periodic N^3 grid split

@@ -37,7 +37,8 @@ enum spidgpu_status {
     SPID_CHECKSUM_MISMATCH = 22,/* "ChecksumMismatch" archive.cpp:92 */
     SPID_COVERAGE_GAP = 23,     /* "CoverageGap"      archive.cpp:285; blocking.cpp:236 */
     SPID_UNSTRUCTURED_NO_INTERP = 24,/* "UnstructuredNoInterp" archive.cpp:291; interp.cpp:47 */
-    SPID_BAD_STREAM_CONFIG = 25,/* "BadStreamConfig"  spid_cli.cpp:248-263 */
+    SPID_BAD_STREAM_CONFIG = 25,/* "BadStreamConfig"  pipeline.cpp:110-113; spid_cli.cpp:248-263 */
+    SPID_SHORT_STREAM = 26,     /* "ShortStream"      pipeline.cpp:246-247 */
     /* codes that exist only on the device path */
     SPID_CUDA_ERROR = 100,      /* "CudaError" */
     SPID_INVALID_ARGUMENT = 101,/* "InvalidArgument" (null pointer, bad leading dim) */

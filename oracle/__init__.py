@@ -36,7 +36,7 @@ STATUS_NAMES = {
     10: "IndexOutOfRange", 11: "GeometryMismatch", 12: "ZeroReference",
     13: "ZeroDenominator", 14: "BadSubsampleSpec", 15: "EmptySketch", 16: "ExtrapolationRequired", 17: "BadGridGeom",
     18: "BlockTooSmall", 19: "BadMagic", 20: "VersionUnsupported", 21: "TruncatedPayload",
-    22: "ChecksumMismatch", 23: "CoverageGap", 24: "UnstructuredNoInterp", 25: "BadStreamConfig",
+    22: "ChecksumMismatch", 23: "CoverageGap", 24: "UnstructuredNoInterp", 25: "BadStreamConfig", 26: "ShortStream",
     100: "CudaError", 101: "InvalidArgument", 102: "ShapeUnsupported", 103: "NoDevice",
 }
 
@@ -331,6 +331,33 @@ class _Ref:
         out = np.empty(nb.value, dtype=np.uint8)
         self.lib.ref_archive_fetch(out.ctypes.data, nb.value)
         return out.tobytes()
+
+    def run_pipeline(self, a, dims, blocks, strides, time_chunk, stage1_rank, stage2_tol=1e-6,
+                     periodic=None, include_boundary=True, workers=1, qoi="", provenance=""):
+        """run_pipeline over the columns of `a` + encode() -> (bytes, stats);
+        stats = [fine_entries_peak, coarse_entries_peak, #stage1, #stage2]."""
+        a = _f64(a)
+        m, n = a.shape
+        nax = len(dims)
+        if self.lib.ref_run_pipeline.argtypes is None:
+            self.lib.ref_run_pipeline.argtypes = [
+                _D, _sz, _sz, _SZ, C.POINTER(C.c_int), _sz, _SZ, _SZ, C.c_int, _sz, _sz, C.c_double,
+                _sz, C.c_char_p, C.c_char_p, _SZ, _SZ, C.c_char_p, _sz]
+        d, p, s, _ = _Port._spec(dims, strides, periodic)
+        b = (C.c_size_t * nax)(*blocks)
+        nb = C.c_size_t(0)
+        stats = (C.c_size_t * 4)()
+        err = C.create_string_buffer(512)
+        if self.lib.ref_run_pipeline(_dp(a), m, n, d, p, nax, b, s, int(include_boundary), time_chunk,
+                                     stage1_rank, stage2_tol, workers, qoi.encode(), provenance.encode(),
+                                     C.byref(nb), stats, err, 512):
+            name, _, what = err.value.decode().partition("|")
+            e = OracleError(name)
+            e.what = what
+            raise e
+        out = np.empty(nb.value, dtype=np.uint8)
+        self.lib.ref_archive_fetch(out.ctypes.data, nb.value)
+        return out.tobytes(), list(stats)
 
     def archive_decompress(self, data):
         b = np.frombuffer(bytes(data), dtype=np.uint8)

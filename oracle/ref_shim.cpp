@@ -368,3 +368,61 @@ std::uint32_t ref_crc32(const std::uint8_t* data, std::size_t length) {
 }
 
 }  // extern "C"
+
+// ---- streaming two-stage pipeline ------------------------------
+#include "spid/pipeline.hpp"
+#include "spid/producer.hpp"
+
+extern "C" {
+
+// run_pipeline (pipeline.cpp:104-294) over the columns of `a` (m x n) with a
+// MatrixProducer (producer.hpp:24-40); encode() of the resulting archive into
+// g_archive. Stats: fine_peak, coarse_peak, stage1 events, stage2 events.
+int ref_run_pipeline(const double* a, std::size_t m, std::size_t n, const std::size_t* dims,
+                     const int* periodic, std::size_t naxes, const std::size_t* blocks,
+                     const std::size_t* strides, int include_boundary, std::size_t time_chunk,
+                     std::size_t stage1_rank, double stage2_tol, std::size_t workers,
+                     const char* qoi, const char* provenance, std::size_t* nbytes,
+                     std::size_t* stats, char* err, std::size_t errlen) {
+    try {
+        std::vector<std::size_t> d(dims, dims + naxes), b(blocks, blocks + naxes),
+            s(strides, strides + naxes);
+        std::vector<bool> p(naxes);
+        for (std::size_t i = 0; i < naxes; ++i) p[i] = periodic[i] != 0;
+        const DenseMatrix am = from_ptr(a, m, n);
+        spid::StreamConfig cfg;
+        cfg.plan = {spid::GridGeom::structured(d, p), b, time_chunk};
+        cfg.strides = s;
+        cfg.include_boundary = include_boundary != 0;
+        cfg.stage1_rank = stage1_rank;
+        cfg.stage2_tol = stage2_tol;
+        cfg.workers = workers;
+        cfg.qoi = qoi ? qoi : "";
+        cfg.provenance = provenance ? provenance : "";
+        spid::MatrixProducer prod(am);
+        const spid::PipelineResult r = spid::run_pipeline(prod, cfg);
+        g_archive = spid::encode(r.archive);
+        *nbytes = g_archive.size();
+        if (stats) {
+            std::size_t s1 = 0, s2 = 0;
+            for (const auto& e : r.events) {
+                s1 += e.kind == spid::TaskEvent::Kind::Stage1Done;
+                s2 += e.kind == spid::TaskEvent::Kind::Stage2Done;
+            }
+            stats[0] = r.buffers.fine_entries_peak;
+            stats[1] = r.buffers.coarse_entries_peak;
+            stats[2] = s1;
+            stats[3] = s2;
+        }
+        return 0;
+    } catch (const spid::Error& e) {
+        if (err && errlen) {
+            std::string msg = e.name() + std::string("|") + e.what();
+            std::strncpy(err, msg.c_str(), errlen - 1);
+            err[errlen - 1] = 0;
+        }
+        return 1;
+    }
+}
+
+}  // extern "C"

@@ -83,6 +83,20 @@ def archive_spec(dims, blocks, strides, periodic=None, mode=ARCHIVE_EXACT, ell=0
                        seed, qoi.encode(), provenance.encode())
 
 
+class StreamConfig(C.Structure):
+    _fields_ = [("naxes", C.c_int32), ("include_boundary", C.c_int32), ("dims", C.c_int64 * 3),
+                ("periodic", C.c_int32 * 3), ("reserved", C.c_int32),
+                ("blocks_per_axis", C.c_int64 * 3), ("strides", C.c_int64 * 3),
+                ("time_chunk", C.c_int64), ("stage1_rank", C.c_int64), ("stage2_tol", C.c_double),
+                ("qoi", C.c_char_p), ("provenance", C.c_char_p)]
+
+
+class StreamStats(C.Structure):
+    _fields_ = [("snapshots", C.c_int64), ("stage1_tasks", C.c_int64), ("stage2_tasks", C.c_int64),
+                ("fine_entries_peak", C.c_int64), ("coarse_entries_peak", C.c_int64),
+                ("stage1_ms", C.c_double), ("stage2_ms", C.c_double)]
+
+
 _vp = C.c_void_p
 _i64 = C.c_int64
 _H = C.c_void_p
@@ -134,6 +148,12 @@ _SIGS = {
     "spidgpu_archive_shape": (C.c_int, [_vp, _i64, _pi64, _pi64, _pi64]),
     "spidgpu_archive_info": (C.c_int, [_H, _vp, _i64, _vp, _i64, _pi64]),
     "spidgpu_archive_decompress": (C.c_int, [_H, _vp, _i64, _vp, _i64, C.c_int32]),
+    "spidgpu_stream_open": (C.c_int, [_H, C.POINTER(StreamConfig), C.POINTER(_vp)]),
+    "spidgpu_stream_push": (C.c_int, [_vp, _vp, _i64, _i64, _i64, C.c_int32]),
+    "spidgpu_stream_finish": (C.c_int, [_vp, _pi64]),
+    "spidgpu_stream_get_stats": (C.c_int, [_vp, C.POINTER(StreamStats)]),
+    "spidgpu_stream_last_error": (C.c_char_p, [_vp]),
+    "spidgpu_stream_close": (C.c_int, [_vp]),
     "spidgpu_field_generate": (C.c_int, [_H, C.POINTER(FieldSpec), _i64, _i64, _vp, _vp, _i64,
                                          _i64, _vp]),
     "spidgpu_row_indices": (C.c_int, [_GS, _vp, _i64, C.POINTER(C.c_int64)]),

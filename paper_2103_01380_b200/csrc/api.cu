@@ -390,7 +390,7 @@ namespace spidgpu {
 // ---- SPID grid specs ----------------------------------------------------------------
 // Validation of SubsampleSpec::strided / GridGeom::structured (grid.cpp:7-20, 62-75).
 int spec_to_dev(spidgpu_handle h, const spidgpu_grid_spec* sp, GridSpecDev* g, int64_t* P,
-                int64_t* Pc, int min_dim) {
+                int64_t* Pc, int min_dim, bool lift) {
     if (!sp) return fail(h, SPID_INVALID_ARGUMENT, "null grid spec");
     if (sp->naxes < 1 || sp->naxes > 3) return fail(h, SPID_BAD_GRID_GEOM, "structured grids have 1 to 3 axes");
     if (sp->nqoi < 1) return fail(h, SPID_BAD_SUBSAMPLE_SPEC, "nqoi must be >= 1");
@@ -412,7 +412,7 @@ int spec_to_dev(spidgpu_handle h, const spidgpu_grid_spec* sp, GridSpecDev* g, i
             const bool extra = g->incl && !g->periodic[ax] && (base - 1) * sp->strides[ax] != sp->dims[ax] - 1;
             // interp.cpp:25-29: fine points past the last coarse point of a
             // non-periodic axis cannot be lifted (raised when M is built)
-            if (!g->periodic[ax] && !extra && (base - 1) * sp->strides[ax] != sp->dims[ax] - 1)
+            if (lift && !g->periodic[ax] && !extra && (base - 1) * sp->strides[ax] != sp->dims[ax] - 1)
                 return fail(h, SPID_EXTRAPOLATION_REQUIRED,
                             "fine point beyond the last coarse point on a non-periodic axis");
             *P *= sp->dims[ax];
@@ -480,6 +480,7 @@ const char* spidgpu_status_name(int status) {
         case SPID_COVERAGE_GAP: return "CoverageGap";
         case SPID_UNSTRUCTURED_NO_INTERP: return "UnstructuredNoInterp";
         case SPID_BAD_STREAM_CONFIG: return "BadStreamConfig";
+        case SPID_SHORT_STREAM: return "ShortStream";
         case SPID_CUDA_ERROR: return "CudaError";
         case SPID_INVALID_ARGUMENT: return "InvalidArgument";
         case SPID_SHAPE_UNSUPPORTED: return "ShapeUnsupported";

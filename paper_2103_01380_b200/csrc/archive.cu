@@ -98,14 +98,17 @@ __device__ __forceinline__ uint64_t get_u64(const uint8_t* p) {
     return v;
 }
 
-// One thread per 8-byte item of a section (item 1 is the coarse byte).
+// One thread per 8-byte item of a section (item 1 is the coarse byte). Items
+// after the coarse byte: nu | union[nu] | k | sel[k] | mc | k | skel[mc*k] |
+// k | n | coeffs[k*n], each a u64 / f64 at payload offset 1 + 8*(item - 2).
 __global__ void pack_blocks_kernel(const PackBlock* __restrict__ blocks, int64_t nblocks,
                                    uint8_t* __restrict__ out) {
     for (int64_t b = blockIdx.y; b < nblocks; b += gridDim.y) {
         const PackBlock d = blocks[b];
-        const int64_t k = d.k, mck = d.mc * d.k, kn = d.k * d.n;
-        const int64_t items = 8 + 2 * k + mck + kn;
-        const int64_t payload = 49 + 16 * k + 8 * mck + 8 * kn;
+        const int64_t k = d.k, nu = d.nu, mck = d.mc * d.k, kn = d.k * d.n;
+        const int64_t items = 8 + nu + k + mck + kn;
+        const int64_t payload = 49 + 8 * nu + 8 * k + 8 * mck + 8 * kn;
+        const int64_t s0 = nu + k + 4;  // first skeleton item (q index)
         for (int64_t it = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; it < items;
              it += static_cast<int64_t>(gridDim.x) * blockDim.x) {
             uint8_t* sec = out + d.sec_off;
@@ -119,26 +122,28 @@ __global__ void pack_blocks_kernel(const PackBlock* __restrict__ blocks, int64_t
             }
             const int64_t q = it - 2;
             uint64_t v;
-            if (q == 0 || q == k + 1) {
-                v = static_cast<uint64_t>(k);
-            } else if (q <= k) {
+            if (q == 0) {
+                v = static_cast<uint64_t>(nu);
+            } else if (q <= nu) {
                 v = static_cast<uint64_t>(d.uni[q - 1]);
-            } else if (q <= 2 * k + 1) {
-                v = static_cast<uint64_t>(d.sel[q - k - 2]);
-            } else if (q == 2 * k + 2) {
-                v = static_cast<uint64_t>(d.mc);
-            } else if (q == 2 * k + 3) {
+            } else if (q == nu + 1) {
                 v = static_cast<uint64_t>(k);
-            } else if (q < 2 * k + 4 + mck) {
-                const uint32_t e = static_cast<uint32_t>(q - (2 * k + 4));
+            } else if (q <= nu + k + 1) {
+                v = static_cast<uint64_t>(d.sel[q - nu - 2]);
+            } else if (q == nu + k + 2) {
+                v = static_cast<uint64_t>(d.mc);
+            } else if (q == nu + k + 3) {
+                v = static_cast<uint64_t>(k);
+            } else if (q < s0 + mck) {
+                const uint32_t e = static_cast<uint32_t>(q - s0);
                 const uint32_t mc = static_cast<uint32_t>(d.mc);
                 v = __double_as_longlong(__ldg(d.skel + static_cast<int64_t>(e / mc) * d.ld_s + e % mc));
-            } else if (q == 2 * k + 4 + mck) {
+            } else if (q == s0 + mck) {
                 v = static_cast<uint64_t>(k);
-            } else if (q == 2 * k + 5 + mck) {
+            } else if (q == s0 + mck + 1) {
                 v = static_cast<uint64_t>(d.n);
             } else {
-                const uint32_t e = static_cast<uint32_t>(q - (2 * k + 6 + mck));
+                const uint32_t e = static_cast<uint32_t>(q - (s0 + mck + 2));
                 const uint32_t kk = static_cast<uint32_t>(k);
                 v = __double_as_longlong(__ldg(d.coeffs + static_cast<int64_t>(e / kk) * d.ld_c + e % kk));
             }

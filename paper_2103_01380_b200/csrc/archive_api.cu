@@ -11,23 +11,13 @@
 #include <string>
 #include <vector>
 
-#include "archive_meta.h"
-#include "context.h"
+#include "archive_internal.h"
 
 using namespace spidgpu;
 
 namespace spidgpu {
 
-namespace {
-
-constexpr uint32_t kVersion = 1;
-constexpr size_t kAlign = 256;
-
 // ---- make_block_domains (proj/src/blocking.cpp:12-104) ------------------------
-struct Seg {
-    int64_t start, len;
-};
-
 int axis_segments(spidgpu_handle h, int64_t dim, int64_t count, std::vector<Seg>* out) {
     if (count < 1 || count > dim)
         return fail(h, SPID_BLOCK_TOO_SMALL, "blocks per axis must lie in [1, axis dim]");
@@ -42,21 +32,6 @@ int axis_segments(spidgpu_handle h, int64_t dim, int64_t count, std::vector<Seg>
     }
     return SPID_OK;
 }
-
-struct Domain {
-    int64_t base;    // global flat index of the block's first point
-    int64_t l[3];    // local dims (unstructured: l[0] = points)
-    int32_t per[3];  // local periodic flags
-};
-
-struct Layout {
-    bool structured = true;
-    int naxes = 1;
-    int64_t dims[3] = {1, 1, 1};
-    int64_t points = 0;
-    std::vector<Domain> doms;
-    std::vector<Seg> segs[3];
-};
 
 int make_domains(spidgpu_handle h, bool structured, int naxes, const int64_t* dims,
                  const int32_t* periodic, int64_t points, const std::vector<int64_t>& blocks,
@@ -104,14 +79,6 @@ int make_domains(spidgpu_handle h, bool structured, int naxes, const int64_t* di
     return SPID_OK;
 }
 
-// Blocks of one local geometry (and, for decompress, one coarse flag) share
-// their row maps and run as one batch.
-struct Group {
-    Domain proto;
-    int32_t coarse = 0;
-    std::vector<int64_t> members;  // block ids, ascending
-};
-
 std::vector<Group> group_blocks(const Layout& L, const std::vector<int32_t>* coarse) {
     std::vector<Group> groups;
     for (int64_t b = 0; b < static_cast<int64_t>(L.doms.size()); ++b) {
@@ -131,15 +98,8 @@ std::vector<Group> group_blocks(const Layout& L, const std::vector<int32_t>* coa
     return groups;
 }
 
-// global offset (relative to the block base) of local flat index l
-inline int64_t globalize(const Layout& L, const Domain& d, int64_t l) {
-    const int64_t i0 = l % d.l[0], i1 = (l / d.l[0]) % d.l[1], i2 = l / (d.l[0] * d.l[1]);
-    return i0 + L.dims[0] * i1 + L.dims[0] * L.dims[1] * i2;
-}
-
-// local SubsampleSpec::strided(local, strides, include_boundary)
 int local_spec(spidgpu_handle h, const Layout& L, const Domain& d, const int64_t* strides,
-               int incl, GridSpecDev* g, int64_t* P, int64_t* Pc) {
+               int incl, GridSpecDev* g, int64_t* P, int64_t* Pc, bool lift) {
     spidgpu_grid_spec sp{};
     sp.naxes = L.naxes;
     sp.include_boundary = incl;
@@ -149,59 +109,12 @@ int local_spec(spidgpu_handle h, const Layout& L, const Domain& d, const int64_t
         sp.strides[ax] = ax < L.naxes ? strides[ax] : 1;
         sp.periodic[ax] = d.per[ax];
     }
-    return spec_to_dev(h, &sp, g, P, Pc, /*min_dim=*/1);
+    return spec_to_dev(h, &sp, g, P, Pc, /*min_dim=*/1, lift);
 }
 
-// Byte arena carved out of one device buffer.
-struct Carve {
-    size_t off = 0;
-    template <class T>
-    size_t take(size_t count) {
-        off = (off + kAlign - 1) / kAlign * kAlign;
-        const size_t o = off;
-        off += sizeof(T) * std::max<size_t>(count, 1);
-        return o;
-    }
-};
+namespace {
 
-// SPIDGPU_TRACE=1: per-phase device times of the archive calls on stderr.
-struct Trace {
-    bool on = std::getenv("SPIDGPU_TRACE") != nullptr;
-    cudaStream_t st;
-    std::vector<std::pair<std::string, cudaEvent_t>> marks;
-    explicit Trace(cudaStream_t s) : st(s) { mark("start"); }
-    void mark(const char* name) {
-        if (!on) return;
-        cudaEvent_t e;
-        cudaEventCreate(&e);
-        cudaEventRecord(e, st);
-        marks.emplace_back(name, e);
-    }
-    ~Trace() {
-        if (!on) return;
-        cudaEventSynchronize(marks.back().second);
-        std::string line = "[spidgpu trace]";
-        for (size_t i = 1; i < marks.size(); ++i) {
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
-            line += " " + marks[i].first + "=" + std::to_string(ms) + "ms";
-        }
-        std::fprintf(stderr, "%s\n", line.c_str());
-        for (auto& m : marks) cudaEventDestroy(m.second);
-    }
-};
-
-template <class T>
-T* at(DevBuf& buf, size_t off) {
-    return reinterpret_cast<T*>(static_cast<uint8_t*>(buf.ptr) + off);
-}
-
-void put_u32(std::vector<uint8_t>& o, uint32_t v) {
-    for (int i = 0; i < 4; ++i) o.push_back(static_cast<uint8_t>(v >> (8 * i)));
-}
-void put_u64(std::vector<uint8_t>& o, uint64_t v) {
-    for (int i = 0; i < 8; ++i) o.push_back(static_cast<uint8_t>(v >> (8 * i)));
-}
+constexpr uint32_t kVersion = kArchiveVersion;
 
 // ---- decode() framing (archive.cpp:37-98, 214-249) --------------------------------
 struct Reader {
@@ -424,6 +337,83 @@ int layout_from_meta(spidgpu_handle h, const ArchiveMetaHost& m, Layout* L) {
 
 }  // namespace
 
+int emit_archive(spidgpu_handle h, Workspace& ws, const ArchiveMetaHost& meta,
+                 std::vector<PackBlock>& pack, cudaStream_t st, Trace* tr, int64_t* nbytes) {
+    // container layout: magic | u32 version | meta section | u64 count | blocks
+    const int64_t nblocks = static_cast<int64_t>(pack.size());
+    const std::string mj = meta_to_json_string(meta);
+    std::vector<uint8_t> head;
+    head.insert(head.end(), {'S', 'P', 'I', 'D'});
+    put_u32(head, kArchiveVersion);
+    put_u64(head, mj.size());
+    head.insert(head.end(), mj.begin(), mj.end());
+    put_u32(head, 0);  // CRC, written on the device
+    put_u64(head, static_cast<uint64_t>(nblocks));
+
+    std::vector<CrcSection> secs(nblocks + 1);
+    secs[0] = {16, static_cast<int64_t>(mj.size())};
+    int64_t off = static_cast<int64_t>(head.size()), max_items = 1;
+    for (int64_t b = 0; b < nblocks; ++b) {
+        PackBlock& d = pack[b];
+        d.sec_off = off;
+        const int64_t payload = 49 + 8 * d.nu + 8 * d.k + 8 * d.mc * d.k + 8 * d.k * d.n;
+        max_items = std::max(max_items, 8 + d.nu + d.k + d.mc * d.k + d.k * d.n);
+        secs[b + 1] = {off + 8, payload};
+        off += 8 + payload + 4;
+    }
+    const int64_t total = off;
+    std::vector<CrcPart> parts;
+    std::vector<int64_t> first_part;
+    crc_plan_parts(secs.data(), static_cast<int64_t>(secs.size()), &parts, &first_part);
+    Carve cc;
+    const size_t o_pack = cc.take<PackBlock>(pack.size());
+    const size_t o_secs = cc.take<CrcSection>(secs.size());
+    const size_t o_crc = cc.take<uint32_t>(secs.size());
+    const size_t o_parts = cc.take<CrcPart>(parts.size());
+    const size_t o_first = cc.take<int64_t>(first_part.size());
+    const size_t o_pcrc = cc.take<uint32_t>(parts.size());
+    CK(h, ws.crc.ensure(cc.off, st));
+    CK(h, ws.bytes.ensure(static_cast<size_t>(total), st));
+    uint8_t* dev = ws.bytes.as<uint8_t>();
+    CK(h, cudaMemcpyAsync(dev, head.data(), head.size(), cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(at<PackBlock>(ws.crc, o_pack), pack.data(), sizeof(PackBlock) * pack.size(),
+                          cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(at<CrcSection>(ws.crc, o_secs), secs.data(), sizeof(CrcSection) * secs.size(),
+                          cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(at<CrcPart>(ws.crc, o_parts), parts.data(), sizeof(CrcPart) * parts.size(),
+                          cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(at<int64_t>(ws.crc, o_first), first_part.data(), sizeof(int64_t) * first_part.size(),
+                          cudaMemcpyHostToDevice, st));
+    if (tr) tr->mark("host-layout");
+    if (nblocks) {
+        CK(h, launch_pack_blocks(at<PackBlock>(ws.crc, o_pack), nblocks, max_items, dev, st));
+        h->launches += 1;
+    }
+    if (tr) tr->mark("pack");
+    CK(h, launch_crc_sections(dev, at<CrcSection>(ws.crc, o_secs), nblocks + 1, at<CrcPart>(ws.crc, o_parts),
+                              static_cast<int64_t>(parts.size()), at<int64_t>(ws.crc, o_first),
+                              at<uint32_t>(ws.crc, o_pcrc), at<uint32_t>(ws.crc, o_crc), dev, st));
+    h->launches += 2;
+    if (tr) tr->mark("crc");
+    // one device-to-host copy of the finished archive into pinned memory
+    if (h->archive_cap < static_cast<size_t>(total)) {
+        CK(h, cudaStreamSynchronize(st));
+        const size_t want = std::max(static_cast<size_t>(total), h->archive_cap * 3 / 2);
+        if (h->archive_pinned) cudaFreeHost(h->archive_pinned);
+        h->archive_pinned = nullptr;
+        h->archive_cap = 0;
+        h->archive_size = 0;
+        CK(h, cudaHostAlloc(reinterpret_cast<void**>(&h->archive_pinned), want, cudaHostAllocDefault));
+        h->archive_cap = want;
+    }
+    CK(h, cudaMemcpyAsync(h->archive_pinned, dev, static_cast<size_t>(total), cudaMemcpyDeviceToHost, st));
+    if (tr) tr->mark("d2h");
+    CK(h, cudaStreamSynchronize(st));
+    h->archive_size = static_cast<size_t>(total);
+    *nbytes = total;
+    return SPID_OK;
+}
+
 }  // namespace spidgpu
 
 extern "C" {
@@ -536,9 +526,6 @@ int spidgpu_archive_compress(spidgpu_handle h, const double* a, int64_t m, int64
         p.o_status = cv.take<int32_t>(p.nb);
         max_items = std::max(max_items, 8 + 2 * p.kcap + p.Pc * p.kcap + p.kcap * n);
     }
-    const size_t o_pack = cv.take<PackBlock>(nblocks);
-    const size_t o_secs = cv.take<CrcSection>(nblocks + 1);
-    const size_t o_crc = cv.take<uint32_t>(nblocks + 1);
     CK(h, ws.bsk.ensure(cv.off, st));
     Trace tr(st);
 
@@ -662,25 +649,13 @@ int spidgpu_archive_compress(spidgpu_handle h, const double* a, int64_t m, int64
     meta.m = static_cast<size_t>(m);
     meta.n = static_cast<size_t>(n);
     meta.provenance = spec->provenance ? spec->provenance : "";
-    const std::string mj = meta_to_json_string(meta);
-    std::vector<uint8_t> head;
-    head.insert(head.end(), {'S', 'P', 'I', 'D'});
-    put_u32(head, kVersion);
-    put_u64(head, mj.size());
-    head.insert(head.end(), mj.begin(), mj.end());
-    put_u32(head, 0);  // CRC, written on the device
-    put_u64(head, static_cast<uint64_t>(nblocks));
-
     std::vector<PackBlock> pack(nblocks);
-    std::vector<CrcSection> secs(nblocks + 1);
-    secs[0] = {16, static_cast<int64_t>(mj.size())};
-    int64_t off = static_cast<int64_t>(head.size());
     for (int64_t b = 0; b < nblocks; ++b) {
         const GPlan& p = plans[gid[b]];
         const int64_t k = rank[b], t = pos[b];
         PackBlock& d = pack[b];
-        d.sec_off = off;
         d.k = k;
+        d.nu = k;
         d.mc = p.Pc;
         d.n = n;
         d.coarse = p.Pc < L.doms[b].l[0] * L.doms[b].l[1] * L.doms[b].l[2] ? 1 : 0;
@@ -690,55 +665,8 @@ int spidgpu_archive_compress(spidgpu_handle h, const double* a, int64_t m, int64
         d.ld_s = p.Pc;
         d.coeffs = at<double>(ws.bsk, p.o_C) + t * p.kcap * n;
         d.ld_c = p.kcap;
-        const int64_t payload = 49 + 16 * k + 8 * p.Pc * k + 8 * k * n;
-        secs[b + 1] = {off + 8, payload};
-        off += 8 + payload + 4;
     }
-    const int64_t total = off;
-    std::vector<CrcPart> parts;
-    std::vector<int64_t> first_part;
-    crc_plan_parts(secs.data(), static_cast<int64_t>(secs.size()), &parts, &first_part);
-    Carve cc;
-    const size_t o_parts = cc.take<CrcPart>(parts.size());
-    const size_t o_first = cc.take<int64_t>(first_part.size());
-    const size_t o_pcrc = cc.take<uint32_t>(parts.size());
-    CK(h, ws.crc.ensure(cc.off, st));
-    CK(h, ws.bytes.ensure(static_cast<size_t>(total), st));
-    uint8_t* dev = ws.bytes.as<uint8_t>();
-    CK(h, cudaMemcpyAsync(dev, head.data(), head.size(), cudaMemcpyHostToDevice, st));
-    CK(h, cudaMemcpyAsync(at<PackBlock>(ws.bsk, o_pack), pack.data(), sizeof(PackBlock) * nblocks,
-                          cudaMemcpyHostToDevice, st));
-    CK(h, cudaMemcpyAsync(at<CrcSection>(ws.bsk, o_secs), secs.data(), sizeof(CrcSection) * secs.size(),
-                          cudaMemcpyHostToDevice, st));
-    CK(h, cudaMemcpyAsync(at<CrcPart>(ws.crc, o_parts), parts.data(), sizeof(CrcPart) * parts.size(),
-                          cudaMemcpyHostToDevice, st));
-    CK(h, cudaMemcpyAsync(at<int64_t>(ws.crc, o_first), first_part.data(), sizeof(int64_t) * first_part.size(),
-                          cudaMemcpyHostToDevice, st));
-    tr.mark("host-layout");
-    CK(h, launch_pack_blocks(at<PackBlock>(ws.bsk, o_pack), nblocks, max_items, dev, st));
-    tr.mark("pack");
-    CK(h, launch_crc_sections(dev, at<CrcSection>(ws.bsk, o_secs), nblocks + 1, at<CrcPart>(ws.crc, o_parts),
-                              static_cast<int64_t>(parts.size()), at<int64_t>(ws.crc, o_first),
-                              at<uint32_t>(ws.crc, o_pcrc), at<uint32_t>(ws.bsk, o_crc), dev, st));
-    h->launches += 3;
-    tr.mark("crc");
-    // one device-to-host copy of the finished archive into pinned memory
-    if (h->archive_cap < static_cast<size_t>(total)) {
-        CK(h, cudaStreamSynchronize(st));
-        const size_t want = std::max(static_cast<size_t>(total), h->archive_cap * 3 / 2);
-        if (h->archive_pinned) cudaFreeHost(h->archive_pinned);
-        h->archive_pinned = nullptr;
-        h->archive_cap = 0;
-        h->archive_size = 0;
-        CK(h, cudaHostAlloc(reinterpret_cast<void**>(&h->archive_pinned), want, cudaHostAllocDefault));
-        h->archive_cap = want;
-    }
-    CK(h, cudaMemcpyAsync(h->archive_pinned, dev, static_cast<size_t>(total), cudaMemcpyDeviceToHost, st));
-    tr.mark("d2h");
-    CK(h, cudaStreamSynchronize(st));
-    h->archive_size = static_cast<size_t>(total);
-    *nbytes = total;
-    return SPID_OK;
+    return emit_archive(h, ws, meta, pack, st, &tr, nbytes);
 }
 
 int spidgpu_archive_fetch(spidgpu_handle h, uint8_t* dst, int64_t cap) {

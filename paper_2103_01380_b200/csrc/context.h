@@ -124,7 +124,7 @@ int to_dev(spidgpu_handle h, DevBuf& buf, const T* src, size_t count, cudaStream
 // Structured grid + strided subsample validation (grid.cpp:7-33, 62-75);
 // min_dim = 2 for GridGeom::structured, 1 for structured_block.
 int spec_to_dev(spidgpu_handle h, const spidgpu_grid_spec* sp, GridSpecDev* g, int64_t* P,
-                int64_t* Pc, int min_dim = 2);
+                int64_t* Pc, int min_dim = 2, bool lift = true);
 std::vector<int64_t> spec_rows(const GridSpecDev& g, int64_t P);
 
 }  // namespace spidgpu

@@ -149,8 +149,9 @@ int64_t crc32_scratch_words(int64_t nbytes);
 struct PackBlock {          // one block section of the archive
     int64_t sec_off;        // archive offset of the section's u64 length field
     int64_t k, mc, n;       // rank, skeleton rows, snapshot columns
+    int64_t nu;             // union index count (== k for batch archives)
     int32_t coarse;
-    const int64_t* uni;     // sorted skeleton indices
+    const int64_t* uni;     // union_indices (sorted)
     const int64_t* sel;     // skeleton indices in selection order
     const double* skel;     // mc x k, ld ld_s
     int64_t ld_s;
@@ -198,6 +199,28 @@ cudaError_t launch_recon_scatter(const double* F, int64_t ldf, int64_t strideF, 
                                  double* out, int64_t ldo, cudaStream_t st);
 cudaError_t launch_nonfinite_blocks(const double* A, int64_t lda, int64_t m, int64_t n,
                                     const BlockGridDev& g, int32_t* flags, cudaStream_t st);
+
+// ---- streaming two-stage compressor (stream.cu) -----------------------------
+struct StreamChunkDev {        // one closed chunk of one geometry group
+    const double* skel;        // nb x kcap x mc: skeleton columns in sorted order
+    const int64_t* sorted_idx; // nb x kcap: chunk-local skeleton indices, ascending
+    const int32_t* sorted_pos; // nb x kcap: their stage-1 selection positions
+    const int64_t* rank;       // nb
+    const double* C0;          // nb x kcap x cols (ld kcap): stage-1 coefficients
+    int64_t kcap, cols, col0;
+};
+cudaError_t launch_sort_pairs(const int64_t* idx, const int64_t* rank, int64_t kcap, int64_t nb,
+                              int64_t* out_idx, int32_t* out_pos, cudaStream_t st);
+cudaError_t launch_concat_union(const StreamChunkDev* chunks, int64_t nchunks, int64_t nb, int64_t mc,
+                                int64_t rmax, double* concat, int64_t* uglob, int32_t* upos,
+                                int64_t* uoff, int64_t* R, cudaStream_t st);
+cudaError_t launch_compose(const StreamChunkDev* chunks, int64_t nchunks, int64_t time_chunk,
+                           int64_t n_total, const double* C1, int64_t kcap2, int64_t rmax,
+                           const int64_t* rank2, const int32_t* upos, const int64_t* uoff, int64_t nb,
+                           double* out, int32_t* bad, cudaStream_t st);
+cudaError_t launch_final_global(const int64_t* idx2, const int64_t* rank2, int64_t kcap2,
+                                const int64_t* uglob, int64_t rmax, int64_t nb, int64_t* out,
+                                cudaStream_t st);
 
 // ---- synthetic fields (fields.cu) ----------------------------------------
 struct FieldParams {

@@ -146,6 +146,51 @@ def archive_cases(ref, port):
     cases["crc_kat"] = np.array([ref.crc32(b"123456789")], dtype=np.int64)
     np.savez_compressed(os.path.join(OUT, "archive_cases.npz"), **cases)
     print("wrote", len(cases), "archive arrays")
+    pipeline_cases(ref, port)
+
+
+# (dims, blocks, strides, periodic, include_boundary, time_chunk, stage1_rank,
+#  stage2_tol, snapshots, input kind)
+PIPELINE_CASES = [
+    ((10, 10), (2, 2), (2, 2), (1, 1), True, 8, 1, 1e-6, 20, "smooth"),
+    ((12, 10), (2, 2), (2, 2), (1, 0), True, 5, 2, 1e-8, 23, "lowrank"),
+    ((13, 11, 9), (3, 2, 2), (2, 3, 1), (0, 1, 0), True, 4, 3, 1e-6, 14, "smooth"),
+    ((17,), (3,), (4,), (0,), True, 3, 2, 1e-10, 10, "lowrank"),
+    ((14,), (1,), (1,), (0,), True, 9, 5, 1e-6, 9, "lowrank"),       # batch-equivalent single chunk
+    ((9, 7, 6), (9, 1, 2), (2, 2, 2), (0, 0, 0), True, 2, 1, 1e-6, 7, "seeded"),
+    ((12, 12, 12), (2, 2, 2), (2, 2, 2), (1, 1, 1), True, 6, 4, 1e-7, 16, "smooth"),
+    ((16, 12), (2, 3), (3, 2), (0, 0), False, 7, 3, 1e-6, 15, "smooth"),  # no boundary pinning
+]
+
+
+def pipeline_cases(ref, port):
+    """Archives of run_pipeline (proj/src/pipeline.cpp:104-294) + encode()."""
+    rng = np.random.default_rng(2024)
+    cases = {}
+    for ci, (dims, blocks, strides, per, incl, T, k, tol, n, kind) in enumerate(PIPELINE_CASES):
+        m = int(np.prod(dims))
+        if kind == "smooth":
+            a = smooth_field(dims, n, 300 + ci)
+        elif kind == "lowrank":
+            a = np.asfortranarray(rng.standard_normal((m, 3)) @ rng.standard_normal((3, n)) +
+                                  1e-4 * rng.standard_normal((m, n)))
+        else:
+            a = port.seeded_matrix(m, n, 700 + ci)
+        data, stats = ref.run_pipeline(a, dims, blocks, strides, T, k, tol, periodic=per,
+                                       include_boundary=incl, qoi=f"p{ci}", provenance="golden pipeline")
+        key = f"pipe_{ci}"
+        cases[key + "_a"] = a
+        cases[key + "_params"] = np.array([len(dims), *dims, *blocks, *strides, *per, int(incl), T, k, n],
+                                          dtype=np.int64)
+        cases[key + "_tol"] = np.array([tol])
+        cases[key + "_bytes"] = np.frombuffer(data, dtype=np.uint8).copy()
+        cases[key + "_stats"] = np.array(stats, dtype=np.int64)
+        try:
+            cases[key + "_out_sha"] = digest(ref.archive_decompress(data))
+        except oracle.OracleError as e:  # e.g. ExtrapolationRequired without boundary pinning
+            cases[key + "_out_err"] = np.frombuffer(e.name.encode(), dtype=np.uint8).copy()
+    np.savez_compressed(os.path.join(OUT, "pipeline_cases.npz"), **cases)
+    print("wrote", len(cases), "pipeline arrays")
 
 
 if __name__ == "__main__":
