@@ -83,8 +83,12 @@ int64_t spidgpu_launch_count(spidgpu_handle h);
 /* Handle options. SPIDGPU_OPT_GENERIC_CPQR = 1 routes column IDs of
  * sketch-sized matrices through the general (shared/global-memory) CPQR
  * kernel instead of the register-resident one; both are bit-exact with the
- * reference, the option exists so tests can cover both. */
+ * reference, the option exists so tests can cover both.
+ * SPIDGPU_OPT_DMMA_SKETCH = 2 runs Philox-Omega sketches on the FP64 DMMA
+ * kernel instead of the exact integer-sliced IMMA kernel (same Omega; the
+ * option exists for tests and A/B measurement). */
 #define SPIDGPU_OPT_GENERIC_CPQR 1
+#define SPIDGPU_OPT_DMMA_SKETCH 2
 int spidgpu_set_option(spidgpu_handle h, int option, int64_t value);
 
 /* =====================================================================

@@ -19,6 +19,7 @@ RULE_FIXED, RULE_TOL, RULE_BLOCKED = 0, 1, 2
 OMEGA_EXPLICIT, OMEGA_PHILOX = 0, 1
 FIELD_TGV4, FIELD_TGV5, FIELD_MULTIMODE = 0, 1, 2
 SPIDGPU_OPT_GENERIC_CPQR = 1
+SPIDGPU_OPT_DMMA_SKETCH = 2
 
 
 class SpidError(RuntimeError):

@@ -99,10 +99,15 @@ int do_sketch(spidgpu_handle h, Workspace& ws, const double* A, int64_t m, int64
         return fail(h, SPID_SHAPE_UNSUPPORTED, "TMA needs 16-byte aligned A, even lda and strideA");
     if (om->mode == SPIDGPU_OMEGA_EXPLICIT && om->ldo < ell)
         return fail(h, SPID_INVALID_ARGUMENT, "ldo < ell");
-    for (int64_t row0 = 0; row0 < ell; row0 += 80) {
-        const int64_t ells = std::min<int64_t>(80, ell - row0);
+    // Philox Omega: exact integer-sliced IMMA kernel (HBM-bound); explicit
+    // Omega (arbitrary fp64 entries): the DMMA kernel
+    const bool i8 = om->mode == SPIDGPU_OMEGA_PHILOX && !h->force_dmma_sketch;
+    const int64_t slice = i8 ? kSketchI8MaxEll : 80;
+    for (int64_t row0 = 0; row0 < ell; row0 += slice) {
+        const int64_t ells = std::min<int64_t>(slice, ell - row0);
         SketchPlan plan;
-        if (!sketch_make_plan(m, n, batch, ells, h->num_sms, &plan))
+        if (!(i8 ? sketch_i8_make_plan(m, n, batch, ells, h->num_sms, &plan)
+                 : sketch_make_plan(m, n, batch, ells, h->num_sms, &plan)))
             return fail(h, SPID_SHAPE_UNSUPPORTED, "no sketch plan");
         CK(h, ws.partial.ensure(plan.partial_elems * sizeof(double), st));
         CUtensorMap tmap;
@@ -137,7 +142,7 @@ int do_sketch(spidgpu_handle h, Workspace& ws, const double* A, int64_t m, int64
         p.Y = Y;
         p.ldy = ldy;
         p.strideY = strideY;
-        CK(h, launch_sketch(p, plan, &tmap, st));
+        CK(h, i8 ? launch_sketch_i8(p, plan, &tmap, st) : launch_sketch(p, plan, &tmap, st));
         h->launches += 2;
     }
     return SPID_OK;
@@ -549,6 +554,7 @@ int spidgpu_set_option(spidgpu_handle h, int option, int64_t value) {
     if (!h) return SPID_INVALID_ARGUMENT;
     switch (option) {
         case SPIDGPU_OPT_GENERIC_CPQR: h->force_generic_cpqr = value != 0; return SPID_OK;
+        case SPIDGPU_OPT_DMMA_SKETCH: h->force_dmma_sketch = value != 0; return SPID_OK;
         default: return SPID_INVALID_ARGUMENT;
     }
 }

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(256) field_kernel(FieldParams p, const double*
                     double val = q[qi];
                     if (p.sigma > 0.0) {
                         double nz[4];
-                        omega_normals4(p.seed ^ 0x5DEECE66DULL, gpt * 8 + qi, 0x9E37u,
+                        normals4_boxmuller(p.seed ^ 0x5DEECE66DULL, gpt * 8 + qi, 0x9E37u,
                                        static_cast<uint32_t>(j >> 2), nz);
                         val += p.sigma * nz[j & 3];
                     }

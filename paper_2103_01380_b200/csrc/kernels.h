@@ -51,10 +51,12 @@ struct SketchPlan {
     int nw;          // N tiles of 8 columns per warp
     int nt;          // columns per CTA tile
     int64_t ntiles_col;   // column tiles per subdomain
-    int64_t nchunk;       // 16-row chunks per subdomain
+    int64_t nchunk;       // row chunks per subdomain
+    int kc_rows;          // rows per chunk (16 DMMA, 32 or 64 integer-sliced)
     int64_t total_chunks; // batch * ntiles_col * nchunk
     int grid;             // CTAs (persistent, balanced contiguous ranges)
     int max_segs;         // partial slots per CTA
+    int halves = 1;       // partial tiles per slot (2: the integer sketch's slice halves)
     size_t smem;
     size_t partial_elems; // doubles of the partial workspace
 };
@@ -76,6 +78,14 @@ bool sketch_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int num_
                       SketchPlan* plan);
 cudaError_t launch_sketch(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap,
                           cudaStream_t stream);
+// fixed-order split-K reduction of the partials into Y (both sketch kernels)
+cudaError_t launch_sketch_reduce(const SketchParams& p, const SketchPlan& plan, cudaStream_t stream);
+// exact integer-sliced sketch for the Philox Omega (sketch_i8.cu)
+constexpr int64_t kSketchI8MaxEll = 48;  // Omega rows per launch; wider sketches are sliced
+bool sketch_i8_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int num_sms,
+                         SketchPlan* plan);
+cudaError_t launch_sketch_i8(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap,
+                             cudaStream_t stream);
 cudaError_t launch_philox_omega(uint64_t seed, int64_t s, int64_t ell, int64_t m, double* out,
                                 int64_t ldo, cudaStream_t stream);
 

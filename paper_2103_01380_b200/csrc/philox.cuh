@@ -5,13 +5,17 @@
 // the sketch kernel never reads Omega from HBM (performance mode), and
 // spidgpu_philox_omega() can materialise the identical matrix for an oracle.
 //
-// Philox4x32-7 (Salmon et al., SC'11): counter {k/4, r, s_lo, s_hi}, key
-// {seed_lo, seed_hi}; the 4 outputs become Omega_s(r, 4*(k/4) + 0..3) via two
-// Box-Muller transforms in fp32 with the SFU intrinsics (the sketch needs a
-// Gaussian-distributed Omega, not fp64-accurate normals), widened to fp64.
+// Philox4x32-7 (Salmon et al., SC'11): counter {k/8, r, s_lo, s_hi}, key
+// {seed_lo, seed_hi}; the 8 16-bit halves of the output select entries of a
+// 4096-quantile table of N(0, 1) rounded to multiples of 1/32 (omega_table.h),
+// so Omega_s(r, k) = Q / 32 with an integer |Q| <= 117. Those entries are
+// exact in fp64 (the DMMA sketch) and in int8 (the integer-sliced sketch,
+// sketch_i8.cu), so both kernels contract the same Omega.
 #pragma once
 
 #include <stdint.h>
+
+#include "omega_table.h"
 
 namespace spidgpu {
 
@@ -48,9 +52,46 @@ __host__ __device__ __forceinline__ Philox4 philox4x32(Philox4 c, uint32_t k0, u
 // SC'11, Table 2) and keeps the producer warps off the sketch's critical path.
 constexpr int kOmegaRounds = 7;
 
-// Four N(0,1) samples for Omega_s(r, 4*kq + 0..3).
-__device__ __forceinline__ void omega_normals4(uint64_t seed, uint64_t s, uint32_t r, uint32_t kq,
-                                               double out[4]) {
+// Quantile table of the discretised Gaussian (tools/gen_omega_table.py). One
+// copy per translation unit (no relocatable device code); 4 KiB.
+static __device__ __align__(16) const int8_t kOmegaQ[1 << kOmegaTableBits] = SPIDGPU_OMEGA_TABLE_INIT;
+
+// The 16-bit Philox outputs of one call: Omega_s(r, 8*ko + j) = Q[u_j >> 4] / 32
+// for j = 0..7, u_j = 16-bit half (j & 1) of output word j / 2. Counter
+// {ko, r, s_lo, s_hi}, key {seed_lo, seed_hi}.
+__device__ __forceinline__ Philox4 omega_bits8(uint64_t seed, uint64_t s, uint32_t r, uint32_t ko) {
+    return philox4x32<kOmegaRounds>(
+        Philox4{ko, r, static_cast<uint32_t>(s), static_cast<uint32_t>(s >> 32)},
+        static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
+}
+
+__device__ __forceinline__ uint32_t omega_u16(const Philox4& v, int j) {
+    const uint32_t w = j < 2 ? v.x : j < 4 ? v.y : j < 6 ? v.z : v.w;
+    return (j & 1) ? (w >> 16) : (w & 0xffffu);
+}
+
+// Eight integer entries Q (Omega = Q / 32) for Omega_s(r, 8*ko + 0..7), read
+// through `tab` (the table in shared memory, or kOmegaQ itself).
+__device__ __forceinline__ void omega_q8(uint64_t seed, uint64_t s, uint32_t r, uint32_t ko,
+                                         const int8_t* tab, int q[8]) {
+    const Philox4 v = omega_bits8(seed, s, r, ko);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) q[j] = tab[omega_u16(v, j) >> (16 - kOmegaTableBits)];
+}
+
+// The same entries as doubles (exact: |Q| <= 117, scaled by 2^-5).
+__device__ __forceinline__ void omega_values8(uint64_t seed, uint64_t s, uint32_t r, uint32_t ko,
+                                              const int8_t* tab, double out[8]) {
+    int q[8];
+    omega_q8(seed, s, r, ko, tab, q);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) out[j] = static_cast<double>(q[j]) * (1.0 / (1 << kOmegaScaleLog2));
+}
+
+// Four N(0,1) samples (Box-Muller in fp32 on the SFU, widened to fp64) from
+// counter {kq, r, s_lo, s_hi}: the additive noise of the synthetic fields.
+__device__ __forceinline__ void normals4_boxmuller(uint64_t seed, uint64_t s, uint32_t r, uint32_t kq,
+                                                   double out[4]) {
     const Philox4 v = philox4x32<kOmegaRounds>(
         Philox4{kq, r, static_cast<uint32_t>(s), static_cast<uint32_t>(s >> 32)},
         static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
@@ -59,7 +100,6 @@ __device__ __forceinline__ void omega_normals4(uint64_t seed, uint64_t s, uint32
     const float u2a = static_cast<float>(v.y) * kInv;
     const float u1b = (static_cast<float>(v.z) + 1.0f) * kInv;
     const float u2b = static_cast<float>(v.w) * kInv;
-    // r = sqrt(-2 ln u) as x * rsqrt(x): MUFU.RSQ, no IEEE-sqrt slow path
     const float xa = fmaxf(-2.0f * __logf(u1a), 1e-30f);
     const float xb = fmaxf(-2.0f * __logf(u1b), 1e-30f);
     const float ra = xa * rsqrtf(xa);

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp >= kWarps) {
         // ------------------------------ producers ------------------------------
         const int pt = tid - kWarps * kWarp;  // 0..63
-        constexpr int kCalls = Cfg::kEllPad * (kKc / 4);  // (row, k-quad) pairs per chunk
+        constexpr int kCalls = Cfg::kEllPad * (kKc / 8);  // (row, k-octet) pairs per chunk
         ChunkPos cp = chunk_pos(lo, nchunk, ntiles_col);  // advanced incrementally
         int slot = 0;
         uint32_t epar = 0;  // parity of the empty-barrier phase being waited on
@@ -128,24 +128,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const uint32_t ob = o_s + slot * Cfg::kOBytes;
             for (int call = pt; call < kCalls; call += kProducerWarps * kWarp) {
-                const int kq = call & 3, r = call >> 2;  // lanes: 4 k-quads x 8 rows
-                double v[4];
-                const int64_t k0 = cp.kc * kKc + 4 * kq;
+                const int ko = call & 1, r = call >> 1;  // lanes: 2 k-octets x 16 rows
+                double v[8];
+                const int64_t k0 = cp.kc * kKc + 8 * ko;
                 if constexpr (OMODE == 1) {
-                    omega_normals4(p.seed, static_cast<uint64_t>(p.sub_base + cp.s),
-                                   static_cast<uint32_t>(p.row0 + r),
-                                   static_cast<uint32_t>(k0 >> 2), v);
-                    if (r >= p.ell) v[0] = v[1] = v[2] = v[3] = 0.0;  // selects, no FP64 math
+                    omega_values8(p.seed, static_cast<uint64_t>(p.sub_base + cp.s),
+                                  static_cast<uint32_t>(p.row0 + r),
+                                  static_cast<uint32_t>(k0 >> 3), kOmegaQ, v);
+                    if (r >= p.ell) {  // selects, no FP64 math
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) v[j] = 0.0;
+                    }
                 } else {
                     const double* src = p.omega + cp.s * p.stride_o + p.row0 + r;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
+                    for (int j = 0; j < 8; ++j)
                         v[j] = (r < p.ell && k0 + j < p.m) ? __ldg(src + (k0 + j) * p.ldo) : 0.0;
                 }
-                // row r, 16B chunks 2kq and 2kq+1, XOR-swizzled by r%8
+                // row r, 16B chunks 4ko..4ko+3, XOR-swizzled by r%8
                 const uint32_t rowb = ob + r * (kKc * 8);
-                sts128(rowb + ((((2 * kq) ^ (r & 7))) << 4), v[0], v[1]);
-                sts128(rowb + ((((2 * kq + 1) ^ (r & 7))) << 4), v[2], v[3]);
+#pragma unroll
+                for (int h = 0; h < 4; ++h)
+                    sts128(rowb + ((((4 * ko + h) ^ (r & 7))) << 4), v[2 * h], v[2 * h + 1]);
             }
             mbar_arrive(&full_o[slot]);
             if (++cp.kc == nchunk) {
@@ -238,7 +242,7 @@ constexpr int kRedMaxNt = 256;
 
 __global__ void __launch_bounds__(256) sketch_reduce_kernel(SketchParams p, int ell_pad, int nt, int64_t nchunk,
                                      int64_t ntiles_col, int64_t total_chunks, int G,
-                                     int max_segs) {
+                                     int max_segs, int halves) {
     __shared__ double slab[kRedRows][kRedMaxNt + 1];
     __shared__ int cfirst, clast;
     const int nslab = (static_cast<int>(p.ell) + kRedRows - 1) / kRedRows;
@@ -266,9 +270,11 @@ __global__ void __launch_bounds__(256) sketch_reduce_kernel(SketchParams p, int 
             const int64_t hi = (static_cast<int64_t>(cc + 1) * total_chunks) / G;
             if (hi <= lo) continue;
             const int segi = static_cast<int>(tile - lo / nchunk);
-            const double* part = p.partial + (static_cast<size_t>(cc) * max_segs + segi) *
-                                                 (static_cast<size_t>(ell_pad) * nt);
-            sum += part[(r0 + rl) * nt + col];
+            for (int hv = 0; hv < halves; ++hv) {
+                const double* part = p.partial + ((static_cast<size_t>(cc) * max_segs + segi) * halves + hv) *
+                                                     (static_cast<size_t>(ell_pad) * nt);
+                sum += part[(r0 + rl) * nt + col];
+            }
         }
         slab[rl][col] = sum;
     }
@@ -282,16 +288,16 @@ __global__ void __launch_bounds__(256) sketch_reduce_kernel(SketchParams p, int 
 
 __global__ void philox_omega_kernel(uint64_t seed, int64_t s, int64_t ell, int64_t m, double* out,
                                     int64_t ldo) {
-    const int64_t nq = (m + 3) / 4;
-    const int64_t total = nq * ell;
+    const int64_t no = (m + 7) / 8;
+    const int64_t total = no * ell;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t r = e % ell, kq = e / ell;
-        double v[4];
-        omega_normals4(seed, static_cast<uint64_t>(s), static_cast<uint32_t>(r),
-                       static_cast<uint32_t>(kq), v);
-        for (int j = 0; j < 4; ++j)
-            if (4 * kq + j < m) out[(4 * kq + j) * ldo + r] = v[j];
+        const int64_t r = e % ell, ko = e / ell;
+        double v[8];
+        omega_values8(seed, static_cast<uint64_t>(s), static_cast<uint32_t>(r),
+                      static_cast<uint32_t>(ko), kOmegaQ, v);
+        for (int j = 0; j < 8; ++j)
+            if (8 * ko + j < m) out[(8 * ko + j) * ldo + r] = v[j];
     }
 }
 
@@ -308,11 +314,7 @@ cudaError_t launch_t(const SketchParams& p, const SketchPlan& plan, const CUtens
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     static_assert(Cfg::kNt <= kRedMaxNt, "reduce slab too narrow");
-    const int nslab = static_cast<int>((p.ell + kRedRows - 1) / kRedRows);
-    sketch_reduce_kernel<<<static_cast<unsigned>(p.batch * plan.ntiles_col * nslab), 256, 0, stream>>>(
-        p, Cfg::kEllPad, Cfg::kNt, plan.nchunk, plan.ntiles_col, plan.total_chunks, plan.grid,
-        plan.max_segs);
-    return cudaGetLastError();
+    return launch_sketch_reduce(p, plan, stream);
 }
 
 // (WM, MTW) by ell_pad; NW picks the column tile
@@ -391,6 +393,7 @@ bool sketch_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int num_
     plan->nw = best_nw;
     plan->nt = 8 * best_nw * wn;
     plan->ntiles_col = (n + plan->nt - 1) / plan->nt;
+    plan->kc_rows = kKc;
     plan->nchunk = (m + kKc - 1) / kKc;
     plan->total_chunks = batch * plan->ntiles_col * plan->nchunk;
     int64_t grid = num_sms;
@@ -406,6 +409,15 @@ bool sketch_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int num_
     return true;
 }
 
+cudaError_t launch_sketch_reduce(const SketchParams& p, const SketchPlan& plan, cudaStream_t stream) {
+    if (plan.nt > kRedMaxNt) return cudaErrorInvalidValue;
+    const int nslab = static_cast<int>((p.ell + kRedRows - 1) / kRedRows);
+    sketch_reduce_kernel<<<static_cast<unsigned>(p.batch * plan.ntiles_col * nslab), 256, 0, stream>>>(
+        p, plan.ell_pad, plan.nt, plan.nchunk, plan.ntiles_col, plan.total_chunks, plan.grid,
+        plan.max_segs, plan.halves);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_sketch(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap,
                           cudaStream_t stream) {
     return p.omega_mode == 1 ? launch_mode<1>(p, plan, tmap, stream)
@@ -414,7 +426,7 @@ cudaError_t launch_sketch(const SketchParams& p, const SketchPlan& plan, const C
 
 cudaError_t launch_philox_omega(uint64_t seed, int64_t s, int64_t ell, int64_t m, double* out,
                                 int64_t ldo, cudaStream_t stream) {
-    const int64_t total = ((m + 3) / 4) * ell;
+    const int64_t total = ((m + 7) / 8) * ell;
     int64_t blocks = (total + 255) / 256;
     if (blocks > 4096) blocks = 4096;
     philox_omega_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(seed, s, ell, m, out, ldo);
