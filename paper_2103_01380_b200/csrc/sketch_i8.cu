@@ -59,7 +59,7 @@ static_assert(kProducers * kProducerRegs + kConsumers * kConsumerRegs <= (kProdu
               "register split exceeds the launch allocation");
 constexpr int kBoxRows = 16;          // 128 B swizzle span of fp64 rows
 constexpr int kPeriodSteps = 2048;    // 65536 rows: 65536 * 117 * 255 < 2^31
-constexpr int kHeadroom = 8;          // exponent bits above the period's first k-step
+constexpr int kHeadroom = 4;          // exponent bits above the period's first stage
 constexpr int kEbMin = 9;             // biased exponent floor (all-zero columns)
 constexpr int kStageBudget = 200 * 1024;
 
@@ -353,23 +353,32 @@ __global__ void __launch_bounds__(kThreads, 1)
             set_exponent(mx);
             psteps = 0;
         }
-        // fixed point: v = rint(x 2^(P-E)) as 64-bit (lo, hi) words
+        // fixed point v = floor(x 2^(P-E)) as 64-bit (lo, hi) words, on the
+        // idle FP64 pipe rather than F2I (XU): t = RD(y + 1.5*2^84) holds
+        // floor(y / 2^32) in its low word; r = RD(y - (t - 1.5*2^84)) lies in
+        // [0, 2^32) with floor(r) exact; RD(r + 2^52) holds floor(r) in its
+        // low word (y = x 2^(P-E) is formed exactly inside the FMAs)
         uint32_t lw[J][8], hw[J][8];
         if (!tiny) {
+            constexpr double kMagHi = 1.5 * 19342813113834066795298816.0;  // 1.5 * 2^84
+            constexpr double kMagLo = 4503599627370496.0;                    // 2^52
 #pragma unroll
             for (int j = 0; j < J; ++j)
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                    const long long v = __double2ll_rn(x[j][e] * scl.x);
-                    lw[j][e] = static_cast<uint32_t>(v);
-                    hw[j][e] = static_cast<uint32_t>(static_cast<unsigned long long>(v) >> 32);
+                    const double t = __fma_rd(x[j][e], scl.x, kMagHi);
+                    // RD keeps r < 2^32 when y - h is inexact (tiny negative y)
+                    const double r = __fma_rd(x[j][e], scl.x, -(t - kMagHi));
+                    const double u = __dadd_rd(r, kMagLo);
+                    hw[j][e] = static_cast<uint32_t>(__double2loint(t));
+                    lw[j][e] = static_cast<uint32_t>(__double2loint(u));
                 }
         } else {
 #pragma unroll
             for (int j = 0; j < J; ++j)
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                    const long long v = __double2ll_rn(x[j][e] * scl.x * scl.y);
+                    const long long v = __double2ll_rd(x[j][e] * scl.x * scl.y);
                     lw[j][e] = static_cast<uint32_t>(v);
                     hw[j][e] = static_cast<uint32_t>(static_cast<unsigned long long>(v) >> 32);
                 }
@@ -485,9 +494,9 @@ cudaError_t launch_sketch_i8(const SketchParams& p, const SketchPlan& plan, cons
                              cudaStream_t stream) {
     if (p.omega_mode != 1) return cudaErrorInvalidValue;
     switch (plan.mt) {
-        case 1: return launch_t<1, 1, 2, 8>(p, plan, tmap, stream);
-        case 2: return launch_t<2, 1, 2, 8>(p, plan, tmap, stream);
-        case 3: return launch_t<3, 1, 2, 8>(p, plan, tmap, stream);
+        case 1: return launch_t<1, 1, 2, 7>(p, plan, tmap, stream);
+        case 2: return launch_t<2, 1, 2, 7>(p, plan, tmap, stream);
+        case 3: return launch_t<3, 1, 2, 7>(p, plan, tmap, stream);
         default: return cudaErrorInvalidValue;
     }
 }
