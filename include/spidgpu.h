@@ -85,10 +85,12 @@ int64_t spidgpu_launch_count(spidgpu_handle h);
  * kernel instead of the register-resident one; both are bit-exact with the
  * reference, the option exists so tests can cover both.
  * SPIDGPU_OPT_DMMA_SKETCH = 2 runs Philox-Omega sketches on the FP64 DMMA
- * kernel instead of the exact integer-sliced IMMA kernel (same Omega; the
- * option exists for tests and A/B measurement). */
+ * kernel, SPIDGPU_OPT_IMMA_SKETCH = 3 on the register-fed IMMA variant of
+ * the exact integer-sliced contraction, instead of its tcgen05 (TMEM) kernel
+ * (same Omega; the options exist for tests and A/B measurement). */
 #define SPIDGPU_OPT_GENERIC_CPQR 1
 #define SPIDGPU_OPT_DMMA_SKETCH 2
+#define SPIDGPU_OPT_IMMA_SKETCH 3
 int spidgpu_set_option(spidgpu_handle h, int option, int64_t value);
 
 /* =====================================================================

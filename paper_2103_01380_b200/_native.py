@@ -20,6 +20,7 @@ OMEGA_EXPLICIT, OMEGA_PHILOX = 0, 1
 FIELD_TGV4, FIELD_TGV5, FIELD_MULTIMODE = 0, 1, 2
 SPIDGPU_OPT_GENERIC_CPQR = 1
 SPIDGPU_OPT_DMMA_SKETCH = 2
+SPIDGPU_OPT_IMMA_SKETCH = 3
 
 
 class SpidError(RuntimeError):

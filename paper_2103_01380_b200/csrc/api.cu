@@ -99,16 +99,21 @@ int do_sketch(spidgpu_handle h, Workspace& ws, const double* A, int64_t m, int64
         return fail(h, SPID_SHAPE_UNSUPPORTED, "TMA needs 16-byte aligned A, even lda and strideA");
     if (om->mode == SPIDGPU_OMEGA_EXPLICIT && om->ldo < ell)
         return fail(h, SPID_INVALID_ARGUMENT, "ldo < ell");
-    // Philox Omega: exact integer-sliced IMMA kernel (HBM-bound); explicit
-    // Omega (arbitrary fp64 entries): the DMMA kernel
-    const bool i8 = om->mode == SPIDGPU_OMEGA_PHILOX && !h->force_dmma_sketch;
-    const int64_t slice = i8 ? kSketchI8MaxEll : 80;
+    // Philox Omega: exact integer-sliced contraction on tcgen05 (UTCIMMA,
+    // HBM-bound), or on register-fed IMMA (SPIDGPU_OPT_IMMA_SKETCH); explicit
+    // Omega (arbitrary fp64 entries) and SPIDGPU_OPT_DMMA_SKETCH: the DMMA kernel
+    enum { K_DMMA, K_IMMA, K_TC };
+    const int kind = om->mode != SPIDGPU_OMEGA_PHILOX || h->force_dmma_sketch ? K_DMMA
+                     : h->force_imma_sketch                                  ? K_IMMA
+                                                                             : K_TC;
+    const int64_t slice = kind == K_TC ? kSketchTcMaxEll : kind == K_IMMA ? kSketchI8MaxEll : 80;
     for (int64_t row0 = 0; row0 < ell; row0 += slice) {
         const int64_t ells = std::min<int64_t>(slice, ell - row0);
         SketchPlan plan;
-        if (!(i8 ? sketch_i8_make_plan(m, n, batch, ells, h->num_sms, &plan)
-                 : sketch_make_plan(m, n, batch, ells, h->num_sms, &plan)))
-            return fail(h, SPID_SHAPE_UNSUPPORTED, "no sketch plan");
+        const bool planned = kind == K_TC ? sketch_tc_make_plan(m, n, batch, ells, h->num_sms, &plan)
+                             : kind == K_IMMA ? sketch_i8_make_plan(m, n, batch, ells, h->num_sms, &plan)
+                                              : sketch_make_plan(m, n, batch, ells, h->num_sms, &plan);
+        if (!planned) return fail(h, SPID_SHAPE_UNSUPPORTED, "no sketch plan");
         CK(h, ws.partial.ensure(plan.partial_elems * sizeof(double), st));
         CUtensorMap tmap;
         cuuint64_t gdim[3] = {static_cast<cuuint64_t>(m), static_cast<cuuint64_t>(n),
@@ -142,7 +147,9 @@ int do_sketch(spidgpu_handle h, Workspace& ws, const double* A, int64_t m, int64
         p.Y = Y;
         p.ldy = ldy;
         p.strideY = strideY;
-        CK(h, i8 ? launch_sketch_i8(p, plan, &tmap, st) : launch_sketch(p, plan, &tmap, st));
+        CK(h, kind == K_TC ? launch_sketch_tc(p, plan, &tmap, st)
+              : kind == K_IMMA ? launch_sketch_i8(p, plan, &tmap, st)
+                               : launch_sketch(p, plan, &tmap, st));
         h->launches += 2;
     }
     return SPID_OK;
@@ -555,6 +562,7 @@ int spidgpu_set_option(spidgpu_handle h, int option, int64_t value) {
     switch (option) {
         case SPIDGPU_OPT_GENERIC_CPQR: h->force_generic_cpqr = value != 0; return SPID_OK;
         case SPIDGPU_OPT_DMMA_SKETCH: h->force_dmma_sketch = value != 0; return SPID_OK;
+        case SPIDGPU_OPT_IMMA_SKETCH: h->force_imma_sketch = value != 0; return SPID_OK;
         default: return SPID_INVALID_ARGUMENT;
     }
 }

@@ -81,7 +81,8 @@ struct spidgpu_context {
     int64_t launches = 0;
     std::string last_error;
     bool force_generic_cpqr = false;  // tests: exercise the shared/global-W kernel too
-    bool force_dmma_sketch = false;   // Philox sketches on the FP64 DMMA kernel instead of IMMA slices
+    bool force_dmma_sketch = false;   // Philox sketches on the FP64 DMMA kernel
+    bool force_imma_sketch = false;   // Philox sketches on register-fed IMMA instead of tcgen05
     uint8_t* archive_pinned = nullptr;  // last archive built by spidgpu_archive_compress
     size_t archive_cap = 0, archive_size = 0;
 };

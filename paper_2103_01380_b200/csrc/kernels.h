@@ -86,6 +86,12 @@ bool sketch_i8_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int n
                          SketchPlan* plan);
 cudaError_t launch_sketch_i8(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap,
                              cudaStream_t stream);
+// the same on tcgen05.mma kind::i8 with TMEM accumulators (sketch_tc.cu)
+constexpr int64_t kSketchTcMaxEll = 64;
+bool sketch_tc_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int num_sms,
+                         SketchPlan* plan);
+cudaError_t launch_sketch_tc(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap,
+                             cudaStream_t stream);
 cudaError_t launch_philox_omega(uint64_t seed, int64_t s, int64_t ell, int64_t m, double* out,
                                 int64_t ldo, cudaStream_t stream);
 

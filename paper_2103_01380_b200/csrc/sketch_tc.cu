@@ -1,0 +1,550 @@
+// sketch_tc.cu -- the performance-mode sketch Y_s = Omega_s * A_s as an EXACT
+// integer-sliced contraction on the 5th-generation tensor cores
+// (tcgen05.mma kind::i8, accumulators in TMEM).
+//
+// Same reference role as sketch_i8.cu (the north star's Gaussian
+// sketch in place of subsample/subsample_column, proj/src/grid.cpp:136-150;
+// CPU restatement matmul(Omega, A), proj/src/dense_matrix.cpp:38-53): the
+// Philox Omega is integer-valued (Omega = Q/32, |Q| <= 117, philox.cuh), each
+// column of A is a fixed-point integer v = rint(x 2^(50-E)) per period (E =
+// exponent of the period's first 32 rows + 3 bits of headroom), formed by ONE
+// DFMA as the mantissa of x 2^(50-E) + 1.5 2^52: its low 56 bits are the
+// offset-binary u = v + 7 2^51, split into 7 unsigned byte slices, each
+// contracted exactly with Q in int32; an 8th MMA against an all-ones tile
+// accumulates sum_k Q, and the offset is removed exactly (int64) at flush. sketch_i8.cu does this with register-fed IMMA.16832, whose issue
+// rate (8 cycles per m16n8k32 per SMSP) bounds it at ~76% of HBM; here the
+// contraction runs on UTCIMMA at 4x the rate, so the kernel is bound by the
+// HBM stream of A.
+//
+// Formulation: Y_s^T (n x ell) = A_s^T (n x m) * Omega_s^T (m x ell), per CTA
+// tile of 128 snapshots: D_t (M=128 snapshots x N=ell_pad, int32, TMEM
+// columns [N t, N t + N)) += slice_t(A^T) (128 x 32, K-major) *
+// Q^T (32 x N, K-major), one MMA per slice per 32-row stage.
+//
+// Warp roles (384 threads, persistent, one CTA per SM, stream-K over
+// (subdomain, 128-column tile, 32-row stage) like sketch.cu):
+//   warp 0      TMA: two 16x128 fp64 boxes (128B swizzle) per stage
+//   warp 1      TMEM allocation; one lane issues the 7 MMAs per stage and
+//               commits them to the slice slot's "empty" mbarrier
+//   warps 2-3   Omega: Philox + quantile table -> K-major int8 tile
+//   warps 4-11  converters, thread (half h, column c): 16 fp64 entries of
+//               rows [16h, 16h+16) -> floor(x 2^(P-E)) on the FP64 pipe
+//               (magic-number split, no F2I) -> 4x4 PRMT byte transposes ->
+//               one 16-byte store per slice into the K-major slice tile.
+//               Warps 4-7 (half 0) own TMEM lanes 0..127 and run the rare
+//               flushes: D -> fp64 partial in HBM (tcgen05.ld 32x32b).
+// A flush happens at segment ends, every 2048 stages (|D| < 2^31) and when
+// a column exceeds its exponent headroom (agreed through per-stage warp
+// votes, published one stage ahead); the
+// stage after a flush is issued with enable-input-d = false.
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "philox.cuh"
+
+namespace spidgpu {
+
+namespace {
+
+constexpr int kThreads = 384;
+constexpr int kConvThreads = 256;     // warps 4..11
+constexpr int kConvWarps = kConvThreads / 32;
+constexpr int kGenThreads = 64;       // warps 2..3
+constexpr int kM = 128;               // snapshots per CTA tile (UMMA M)
+constexpr int kRows = 32;             // rows of A per stage (UMMA K for int8)
+constexpr int kSlices = 7;            // byte slices of the offset-binary fixed point
+constexpr int kP = 50;                // v = rint(x 2^(P-E)), |v| < 2^50 within the headroom
+constexpr int kHeadroom = 3;
+// t = RN(x 2^(P-E) + 1.5 2^52) holds v in its mantissa: the low 56 bits of
+// t's bit pattern are u = v + kOffset (the exponent field 0x433 contributes
+// its low nibble 3 at bit 52), an unsigned 7-byte integer while |v| < 2^51
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+constexpr int kOffsetHi = 7 << 19;             // kOffset = 7 * 2^51 = kOffsetHi * 2^32
+constexpr uint32_t kMagicHi = 0x43300000u;     // hi word of t while v is representable
+constexpr int kEbMin = 9;
+constexpr int kPeriodStages = 2048;   // 65536 rows: 65536 * 117 * 255 < 2^31
+constexpr int kBoxBytes = 16 * kM * 8;              // 16 rows x 128 columns fp64
+constexpr int kAStageBytes = 2 * kBoxBytes;         // 32 KB
+constexpr int kAStages = 4;
+constexpr int kSliceBytes = kM * kRows;             // 4 KB per slice tile
+constexpr int kBStages = 3;
+
+template <int NPAD>
+struct TcCfg {
+    static constexpr int kOmegaBytes = NPAD * kRows;
+    static constexpr int kBStageBytes = kSlices * kSliceBytes + kOmegaBytes;
+    // D_0..D_6 (slices) and D_7 = sum_k Q (all-ones A tile): the offset correction
+    static constexpr int kTmemCols = (kSlices + 1) * NPAD <= 256 ? 256 : 512;
+    // layout: A ring | B ring | ebx[2][128] | flags | barriers
+    static constexpr size_t kOffB = static_cast<size_t>(kAStages) * kAStageBytes;
+    static constexpr size_t kOffMisc = kOffB + static_cast<size_t>(kBStages) * kBStageBytes;
+    // agreement slots: [2][2 halves][128] column maxima + [2][8] warp votes; Omega table; flags
+    static constexpr size_t kMiscBytes = 2 * 2 * 128 * 4 + 2 * kConvWarps * 4 + 4096 + 64 + 128;
+    static constexpr size_t kOffBar = (kOffMisc + kMiscBytes + 7) & ~size_t(7);
+    static constexpr size_t kSmem = 1024 + kOffBar + 8 * (2 * kAStages + 2 * kBStages + 2) + 16;
+};
+
+struct ChunkPos {
+    int s, ct, kc;  // subdomain, column tile, 32-row stage
+};
+
+__device__ __forceinline__ ChunkPos chunk_pos(int64_t g, int64_t nchunk, int64_t ntiles_col) {
+    const int64_t tile = g / nchunk;
+    return ChunkPos{static_cast<int>(tile / ntiles_col), static_cast<int>(tile % ntiles_col),
+                    static_cast<int>(g % nchunk)};
+}
+
+__device__ __forceinline__ void advance(ChunkPos& cp, int nchunk, int ntiles_col) {
+    if (++cp.kc == nchunk) {
+        cp.kc = 0;
+        if (++cp.ct == ntiles_col) {
+            cp.ct = 0;
+            ++cp.s;
+        }
+    }
+}
+
+__device__ __forceinline__ void sts64u(uint32_t addr, uint32_t a, uint32_t b) {
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};\n" ::"r"(addr), "r"(a), "r"(b) : "memory");
+}
+
+__device__ __forceinline__ void sts128u(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    // K-major, no swizzle (canonical interleave): core matrices of 8 rows x
+    // 16 B, row groups SBO apart, the two 16-byte K halves LBO apart;
+    // version 1 (tcgen05), layout type 0
+    return static_cast<uint64_t>((addr >> 4) & 0x3fffu) |
+           (static_cast<uint64_t>((lbo >> 4) & 0x3fffu) << 16) |
+           (static_cast<uint64_t>((sbo >> 4) & 0x3fffu) << 32) | (1ull << 46);
+}
+
+// kind::i8 instruction descriptor: D s32, A (slices) u8 or s8, B (Q) s8, both K-major
+__host__ __device__ constexpr uint32_t idesc_i8(int n, bool a_signed) {
+    return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+           (static_cast<uint32_t>(kM >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+__device__ __forceinline__ int column_eb(uint32_t mg) {
+    const int eb = static_cast<int>(mg >> 20) + 1 + kHeadroom;
+    return eb < kEbMin ? kEbMin : (eb > 2047 ? 2047 : eb);
+}
+
+// 2^(P - E) as two normal doubles (tiny columns need more than 2^1023)
+__device__ __forceinline__ double2 fix_scale(int eb) {
+    const int d = kP + 1023 - eb;
+    const int d1 = d > 1000 ? 1000 : d;
+    return make_double2(__longlong_as_double(static_cast<long long>(d1 + 1023) << 52),
+                        __longlong_as_double(static_cast<long long>(d - d1 + 1023) << 52));
+}
+
+// 2^(E - P) / 32, likewise split
+__device__ __forceinline__ double2 unfix_scale(int eb) {
+    const int e = eb - 1023 - kP - kOmegaScaleLog2;
+    const int e1 = e < -1000 ? -1000 : e;
+    return make_double2(__longlong_as_double(static_cast<long long>(e1 + 1023) << 52),
+                        __longlong_as_double(static_cast<long long>(e - e1 + 1023) << 52));
+}
+
+template <int NPAD>
+__global__ void __launch_bounds__(kThreads, 1)
+    sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchParams p, int64_t nchunk,
+                     int64_t ntiles_col, int64_t total_chunks, int max_segs) {
+    using Cfg = TcCfg<NPAD>;
+    extern __shared__ unsigned char smem_raw[];
+    const uint32_t raw_s = smem_u32(smem_raw);
+    const uint32_t base_s = (raw_s + 1023u) & ~1023u;
+    unsigned char* base = smem_raw + (base_s - raw_s);
+    const uint32_t a_s = base_s;
+    const uint32_t b_s = base_s + static_cast<uint32_t>(Cfg::kOffB);
+    uint32_t* mxs = reinterpret_cast<uint32_t*>(base + Cfg::kOffMisc);            // [2][2][128]
+    uint32_t* votes = mxs + 2 * 2 * 128;                                          // [2][8]
+    int8_t* tab = reinterpret_cast<int8_t*>(votes + 2 * kConvWarps);              // 4096
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tab + 4096);
+    // one all-ones 8x16 core matrix; with LBO = SBO = 0 it reads as a 128 x 32 all-ones A tile
+    const uint32_t ones_s = smem_u32(tab + 4096 + 64);
+    uint32_t* acc_flag = tmem_slot + 1;                                           // [kBStages]
+    uint64_t* a_full = reinterpret_cast<uint64_t*>(base + Cfg::kOffBar);
+    uint64_t* a_empty = a_full + kAStages;
+    uint64_t* b_full = a_empty + kAStages;
+    uint64_t* b_empty = b_full + kBStages;
+    uint64_t* agree = b_empty + kBStages;  // [2]: converter warps published a stage's maxima/votes
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t G = gridDim.x, c = blockIdx.x;
+    const int64_t lo = (c * total_chunks) / G, hi = ((c + 1) * total_chunks) / G;
+    const int niter = static_cast<int>(hi - lo);
+    if (niter <= 0) return;
+
+    for (int i = tid; i < 1024; i += kThreads)
+        reinterpret_cast<int*>(tab)[i] = reinterpret_cast<const int*>(kOmegaQ)[i];
+    for (int i = tid; i < 32; i += kThreads) reinterpret_cast<uint32_t*>(tab + 4096 + 64)[i] = 0x01010101u;
+    fence_proxy_async();
+    if (tid == 0) {
+        prefetch_tmap(&tmap);
+        for (int i = 0; i < kAStages; ++i) {
+            mbar_init(&a_full[i], 1);
+            mbar_init(&a_empty[i], kConvThreads / 32);
+        }
+        for (int i = 0; i < kBStages; ++i) {
+            mbar_init(&b_full[i], (kConvThreads + kGenThreads) / 32);
+            mbar_init(&b_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) mbar_init(&agree[i], kConvWarps);
+        fence_barrier_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                     "n"(Cfg::kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------ TMA producer ------------------------------
+        if (lane == 0) {
+            ChunkPos cp = chunk_pos(lo, nchunk, ntiles_col);
+            for (int it = 0; it < niter; ++it) {
+                const int sl = it % kAStages;
+                if (it >= kAStages) mbar_wait(&a_empty[sl], ((it / kAStages) - 1) & 1);
+                mbar_arrive_expect_tx(&a_full[sl], kAStageBytes);
+#pragma unroll
+                for (int b = 0; b < 2; ++b)
+                    tma_load_3d(base + sl * kAStageBytes + b * kBoxBytes, &tmap, &a_full[sl],
+                                static_cast<int>(cp.kc * kRows + 16 * b), static_cast<int>(cp.ct * kM),
+                                static_cast<int>(cp.s));
+                advance(cp, static_cast<int>(nchunk), static_cast<int>(ntiles_col));
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------ MMA issuer ------------------------------
+        if (lane == 0) {
+            constexpr uint32_t kIdU = idesc_i8(NPAD, false);
+            const uint64_t ones_desc = smem_desc(ones_s, 0, 0);
+            for (int it = 0; it < niter; ++it) {
+                const int sl = it % kBStages;
+                mbar_wait(&b_full[sl], (it / kBStages) & 1);
+                tc_fence_after();
+                const uint32_t acc = acc_flag[sl];
+                const uint32_t st = b_s + sl * Cfg::kBStageBytes;
+                const uint64_t bdesc = smem_desc(st + kSlices * kSliceBytes, NPAD * 16, 128);
+#pragma unroll
+                for (int t = 0; t < kSlices; ++t)
+                    umma_i8(tmem + NPAD * t, smem_desc(st + t * kSliceBytes, kM * 16, 128), bdesc, kIdU, acc);
+                umma_i8(tmem + NPAD * kSlices, ones_desc, bdesc, kIdU, acc);
+                umma_commit(&b_empty[sl]);
+            }
+        }
+    } else if (warp < 4) {
+        // ------------------------------ Omega tiles ------------------------------
+        const int gt = tid - 64;  // 0..63
+        ChunkPos cp = chunk_pos(lo, nchunk, ntiles_col);
+        for (int it = 0; it < niter; ++it) {
+            const int sl = it % kBStages;
+            if (it >= kBStages) mbar_wait(&b_empty[sl], ((it / kBStages) - 1) & 1);
+            const uint32_t ot = b_s + sl * Cfg::kBStageBytes + kSlices * kSliceBytes;
+            const uint32_t ko = static_cast<uint32_t>((cp.kc * kRows) >> 3);
+            for (int task = gt; task < 2 * NPAD; task += kGenThreads) {
+                const int r = task % NPAD, h = task / NPAD;  // row, 16-byte K half
+                uint32_t w[4] = {0u, 0u, 0u, 0u};
+                if (r < p.ell) {
+#pragma unroll
+                    for (int o = 0; o < 2; ++o) {
+                        int q[8];
+                        omega_q8(p.seed, static_cast<uint64_t>(p.sub_base + cp.s), static_cast<uint32_t>(p.row0 + r),
+                                 ko + 2 * h + o, tab, q);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) w[2 * o + e / 4] |= static_cast<uint32_t>(q[e] & 0xff) << (8 * (e & 3));
+                    }
+                }
+                sts128u(ot + h * (NPAD * 16) + r * 16, w[0], w[1], w[2], w[3]);
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&b_full[sl]);
+            advance(cp, static_cast<int>(nchunk), static_cast<int>(ntiles_col));
+        }
+    } else {
+        // ------------------------------ converters ------------------------------
+        // Decoupled warps: the per-stage decisions (flush? new exponents?)
+        // need every warp's overflow vote and both halves' column maxima.
+        // A warp publishes stage it+1's (agree[] mbarrier, one arrival per
+        // warp) before converting stage it, and reads it one stage later, so
+        // the agreement never phase-locks the warps: their FP64, ALU and
+        // shared-memory phases overlap.
+        const int ci = tid - 128;
+        const int half = ci >> 7, col = ci & 127;  // half 0 = warps 4..7 = TMEM lanes 0..127
+        const int cw = warp - 4;
+        int eb = kEbMin, poison = 0;
+        uint32_t thr = 0;
+        double sclx = 0.0, scly = 1.0;
+        bool tiny = false;
+        int seg = 0;
+        bool first = true, pending = false;  // pending: D holds unflushed stages
+        int psteps = 0;
+        ChunkPos cp = chunk_pos(lo, nchunk, ntiles_col);
+        const int nch = static_cast<int>(nchunk), ntc = static_cast<int>(ntiles_col);
+
+        // wait until the MMAs of stage `it` (and all earlier) are complete
+        auto wait_mma = [&](int it) {
+            mbar_wait(&b_empty[it % kBStages], (it / kBStages) & 1);
+            tc_fence_after();
+        };
+        // D (all columns) -> fp64 partial of segment `seg`, with this
+        // column's exponent; half 0 threads own TMEM lane `col`
+        auto flush = [&](bool final_flush) {
+            if (half == 0) {
+                double* part = p.partial + (static_cast<size_t>(c) * max_segs + seg) *
+                                               (static_cast<size_t>(NPAD) * kM);
+                const double2 u = unfix_scale(eb);
+                const uint32_t lane_base = static_cast<uint32_t>(cw * 32) << 16;
+#pragma unroll 1
+                for (int g0 = 0; g0 < NPAD; g0 += 8) {
+                    // exact: sum_t 2^(8t) D_t - kOffset * D_7 as hi * 2^32 + lo
+                    long long lo64[8], hi64[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) lo64[j] = hi64[j] = 0;
+#pragma unroll
+                    for (int t = 0; t <= kSlices; ++t) {
+                        uint32_t v[8];
+                        tmem_ld8(tmem + lane_base + NPAD * t + g0, v);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const long long d = static_cast<int>(v[j]);
+                            if (t < 4)
+                                lo64[j] += d * (1LL << (8 * t));
+                            else if (t < kSlices)
+                                hi64[j] += d * (1LL << (8 * (t - 4)));
+                            else
+                                hi64[j] -= d * kOffsetHi;
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        double val = fma(static_cast<double>(hi64[j]), 4294967296.0, static_cast<double>(lo64[j])) *
+                                     u.x * u.y;
+                        if (final_flush && poison) val = __longlong_as_double(0x7ff8000000000000LL);
+                        double* dst = part + static_cast<size_t>(g0 + j) * kM + col;
+                        *dst = first ? val : *dst + val;
+                    }
+                }
+                tc_fence_before();
+            }
+            first = false;
+        };
+        // stage it's 16 rows [16 half, +16) of column col: 8 conflict-free 16B loads
+        auto load = [&](int it, double (&xv)[16]) {
+            const int sa = it % kAStages;
+            mbar_wait(&a_full[sa], (it / kAStages) & 1);
+            const uint32_t cb = a_s + sa * kAStageBytes + half * kBoxBytes + col * 128;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const double2 v = lds128(cb + ((j ^ (col & 7)) << 4));
+                xv[2 * j] = v.x;
+                xv[2 * j + 1] = v.y;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&a_empty[sa]);
+        };
+        // publish stage it's column maximum and this warp's overflow vote
+        auto publish = [&](int it, const double (&xv)[16]) {
+            uint32_t mx = 0;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) mx = max(mx, static_cast<uint32_t>(__double2hiint(xv[e])) & 0x7fffffffu);
+            const int g = it & 1;
+            mxs[(g * 2 + half) * 128 + col] = mx;
+            const bool w = __any_sync(0xffffffffu, mx >= thr);
+            if (lane == 0) votes[g * kConvWarps + cw] = w ? 1u : 0u;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&agree[g]);
+        };
+
+        // one stage: decide (using the published agreement), publish the
+        // next stage, convert this one into the slice tiles
+        auto step = [&](int it, const double (&xc)[16], double (&xn)[16]) {
+            const int g = it & 1;
+            mbar_wait(&agree[g], (it >> 1) & 1);
+            bool ovf = false;
+#pragma unroll
+            for (int w = 0; w < kConvWarps; ++w) ovf = ovf || votes[g * kConvWarps + w] != 0u;
+            const uint32_t mg = max(mxs[(g * 2) * 128 + col], mxs[(g * 2 + 1) * 128 + col]);
+            const bool fresh = it == 0 || cp.kc == 0 || psteps >= kPeriodStages;
+            uint32_t accumulate = 1;
+            if (fresh || ovf) {  // CTA-uniform
+                if (pending) {   // flush the stages accumulated so far
+                    wait_mma(it - 1);
+                    flush(cp.kc == 0);  // final (poison -> NaN) if the previous stage closed its segment
+                    if (cp.kc == 0) {
+                        ++seg;
+                        first = true;
+                    }
+                }
+                if (it == 0 || cp.kc == 0) poison = 0;
+                if (mg >= 0x7ff00000u) poison = 1;
+                eb = column_eb(mg);
+                // |x| < 2^(E+1) keeps |v| < 2^51: u = v + kOffset stays a 7-byte integer
+                thr = poison ? 0xffffffffu : (eb >= 2046 ? 0x7ff00000u : static_cast<uint32_t>(eb + 1) << 20);
+                const double2 sc2 = fix_scale(eb);
+                sclx = sc2.x;
+                scly = sc2.y;
+                tiny = __any_sync(0xffffffffu, scly != 1.0);
+                psteps = 0;
+                accumulate = 0;
+            }
+            if (it + 1 < niter) {
+                load(it + 1, xn);
+                publish(it + 1, xn);
+            }
+            // one DFMA per entry: t = RN(x 2^(P-E) + 1.5 2^52); its low 56 bits
+            // are u = rint(x 2^(P-E)) + kOffset (offset binary, 7 unsigned bytes)
+            uint32_t lw[16], hw[16];
+            if (!tiny) {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    const double t = fma(xc[e], sclx, kMagic);
+                    hw[e] = static_cast<uint32_t>(__double2hiint(t));
+                    lw[e] = static_cast<uint32_t>(__double2loint(t));
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    const double t = fma(xc[e] * sclx, scly, kMagic);
+                    hw[e] = static_cast<uint32_t>(__double2hiint(t));
+                    lw[e] = static_cast<uint32_t>(__double2loint(t));
+                }
+            }
+            uint32_t sw[kSlices][4];
+#pragma unroll
+            for (int g4 = 0; g4 < 4; ++g4) {
+                const uint32_t* wl = lw + 4 * g4;
+                const uint32_t* wh = hw + 4 * g4;
+                {
+                    const uint32_t t0 = __byte_perm(wl[0], wl[1], 0x5140), t1 = __byte_perm(wl[0], wl[1], 0x7362);
+                    const uint32_t t2 = __byte_perm(wl[2], wl[3], 0x5140), t3 = __byte_perm(wl[2], wl[3], 0x7362);
+                    sw[0][g4] = __byte_perm(t0, t2, 0x5410);
+                    sw[1][g4] = __byte_perm(t0, t2, 0x7632);
+                    sw[2][g4] = __byte_perm(t1, t3, 0x5410);
+                    sw[3][g4] = __byte_perm(t1, t3, 0x7632);
+                }
+                {
+                    const uint32_t t0 = __byte_perm(wh[0], wh[1], 0x5140), t1 = __byte_perm(wh[0], wh[1], 0x7362);
+                    const uint32_t t2 = __byte_perm(wh[2], wh[3], 0x5140), t3 = __byte_perm(wh[2], wh[3], 0x7362);
+                    sw[4][g4] = __byte_perm(t0, t2, 0x5410);
+                    sw[5][g4] = __byte_perm(t0, t2, 0x7632);
+                    sw[6][g4] = __byte_perm(t1, t3, 0x5410);
+                }
+            }
+            // the slice slot is free once the MMAs that read it completed
+            const int sb = it % kBStages;
+            if (it >= kBStages) mbar_wait(&b_empty[sb], ((it / kBStages) - 1) & 1);
+            const uint32_t st = b_s + sb * Cfg::kBStageBytes + half * (kM * 16) + col * 16;
+#pragma unroll
+            for (int t = 0; t < kSlices; ++t) sts128u(st + t * kSliceBytes, sw[t][0], sw[t][1], sw[t][2], sw[t][3]);
+            if (ci == 0) acc_flag[sb] = accumulate;
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&b_full[sb]);
+            pending = true;
+            ++psteps;
+            advance(cp, nch, ntc);
+        };
+
+        double xa[16], xb[16];
+        load(0, xa);
+        publish(0, xa);
+        for (int it = 0; it < niter; it += 2) {
+            step(it, xa, xb);
+            if (it + 1 < niter) step(it + 1, xb, xa);
+        }
+        // final flush of the last segment
+        wait_mma(niter - 1);
+        flush(true);
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(Cfg::kTmemCols));
+    }
+}
+
+template <int NPAD>
+cudaError_t launch_t(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap, cudaStream_t stream) {
+    using Cfg = TcCfg<NPAD>;
+    static_assert(Cfg::kSmem <= 227 * 1024, "shared memory budget");
+    auto kern = sketch_tc_kernel<NPAD>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::kSmem));
+    if (e != cudaSuccess) return e;
+    kern<<<plan.grid, kThreads, Cfg::kSmem, stream>>>(*tmap, p, plan.nchunk, plan.ntiles_col, plan.total_chunks,
+                                                      plan.max_segs);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_sketch_reduce(p, plan, stream);
+}
+
+}  // namespace
+
+bool sketch_tc_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int num_sms, SketchPlan* plan) {
+    if (m < 1 || n < 1 || batch < 1 || ell < 1 || ell > kSketchTcMaxEll) return false;
+    plan->ell_pad = static_cast<int>(16 * ((ell + 15) / 16));
+    plan->mt = plan->ell_pad / 16;
+    plan->nw = 1;
+    plan->nt = kM;
+    plan->ntiles_col = (n + kM - 1) / kM;
+    plan->kc_rows = kRows;
+    plan->nchunk = (m + kRows - 1) / kRows;
+    plan->total_chunks = batch * plan->ntiles_col * plan->nchunk;
+    int64_t grid = num_sms;
+    if (grid > plan->total_chunks) grid = plan->total_chunks;
+    plan->grid = static_cast<int>(grid);
+    const int64_t per = (plan->total_chunks + grid - 1) / grid;
+    plan->max_segs = static_cast<int>(per / plan->nchunk + 2);
+    plan->smem = 0;
+    plan->partial_elems = static_cast<size_t>(grid) * plan->max_segs * plan->ell_pad * plan->nt;
+    return true;
+}
+
+cudaError_t launch_sketch_tc(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap,
+                             cudaStream_t stream) {
+    if (p.omega_mode != 1) return cudaErrorInvalidValue;
+    switch (plan.ell_pad) {
+        case 16: return launch_t<16>(p, plan, tmap, stream);
+        case 32: return launch_t<32>(p, plan, tmap, stream);
+        case 48: return launch_t<48>(p, plan, tmap, stream);
+        case 64: return launch_t<64>(p, plan, tmap, stream);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace spidgpu
