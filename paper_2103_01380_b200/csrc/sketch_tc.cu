@@ -21,22 +21,22 @@
 // columns [N t, N t + N)) += slice_t(A^T) (128 x 32, K-major) *
 // Q^T (32 x N, K-major), one MMA per slice per 32-row stage.
 //
-// Warp roles (384 threads, persistent, one CTA per SM, stream-K over
+// Warp roles (256 threads, persistent, one CTA per SM, stream-K over
 // (subdomain, 128-column tile, 32-row stage) like sketch.cu):
-//   warp 0      TMA: two 16x128 fp64 boxes (128B swizzle) per stage
-//   warp 1      TMEM allocation; one lane issues the 7 MMAs per stage and
-//               commits them to the slice slot's "empty" mbarrier
-//   warps 2-3   Omega: Philox + quantile table -> K-major int8 tile
-//   warps 4-11  converters, thread (half h, column c): 16 fp64 entries of
-//               rows [16h, 16h+16) -> floor(x 2^(P-E)) on the FP64 pipe
-//               (magic-number split, no F2I) -> 4x4 PRMT byte transposes ->
-//               one 16-byte store per slice into the K-major slice tile.
-//               Warps 4-7 (half 0) own TMEM lanes 0..127 and run the rare
-//               flushes: D -> fp64 partial in HBM (tcgen05.ld 32x32b).
-// A flush happens at segment ends, every 2048 stages (|D| < 2^31) and when
-// a column exceeds its exponent headroom (agreed through per-stage warp
-// votes, published one stage ahead); the
-// stage after a flush is issued with enable-input-d = false.
+//   warps 0-3   Omega: Philox + quantile table -> K-major int8 tile, one
+//               warp per SMSP; warp 0's lane 0 also keeps the A ring full
+//               (two 16x128 fp64 TMA boxes, 128B swizzle, per stage), warp
+//               1 allocates TMEM and its lane 0 issues the 8 MMAs per stage
+//               (one stage behind), committed to the slot's "empty" mbarrier
+//   warps 4-7   converters, one per TMEM lane quarter; thread = column c:
+//               its 32 fp64 entries of the stage -> one DFMA each (offset-
+//               binary fixed point, below) -> 4x4 PRMT byte transposes ->
+//               one 16-byte store per slice and K half into the K-major
+//               slice tiles. The thread owns D row c: its rare flushes read
+//               the row (tcgen05.ld 32x32b) into the fp64 partial and zero
+//               it (tcgen05.st), without involving any other warp.
+// A warp flushes its rows at segment ends, every 2048 stages (|D| < 2^31)
+// and when one of its columns exceeds its exponent headroom.
 #include <math.h>
 
 #include "common.cuh"
@@ -47,10 +47,9 @@ namespace spidgpu {
 
 namespace {
 
-constexpr int kThreads = 384;
-constexpr int kConvThreads = 256;     // warps 4..11
-constexpr int kConvWarps = kConvThreads / 32;
-constexpr int kGenThreads = 64;       // warps 2..3
+constexpr int kThreads = 256;
+constexpr int kConvWarps = 4;         // warps 4..7: one per TMEM lane quarter
+constexpr int kGenWarps = 4;          // warps 0..3 (one per SMSP)
 constexpr int kM = 128;               // snapshots per CTA tile (UMMA M)
 constexpr int kRows = 32;             // rows of A per stage (UMMA K for int8)
 constexpr int kSlices = 7;            // byte slices of the offset-binary fixed point
@@ -79,10 +78,10 @@ struct TcCfg {
     // layout: A ring | B ring | ebx[2][128] | flags | barriers
     static constexpr size_t kOffB = static_cast<size_t>(kAStages) * kAStageBytes;
     static constexpr size_t kOffMisc = kOffB + static_cast<size_t>(kBStages) * kBStageBytes;
-    // agreement slots: [2][2 halves][128] column maxima + [2][8] warp votes; Omega table; flags
-    static constexpr size_t kMiscBytes = 2 * 2 * 128 * 4 + 2 * kConvWarps * 4 + 4096 + 64 + 128;
+    // Omega table; TMEM slot; all-ones core matrix
+    static constexpr size_t kMiscBytes = 4096 + 64 + 128;
     static constexpr size_t kOffBar = (kOffMisc + kMiscBytes + 7) & ~size_t(7);
-    static constexpr size_t kSmem = 1024 + kOffBar + 8 * (2 * kAStages + 2 * kBStages + 2) + 16;
+    static constexpr size_t kSmem = 1024 + kOffBar + 8 * (2 * kAStages + 2 * kBStages) + 16;
 };
 
 struct ChunkPos {
@@ -149,6 +148,11 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
                  : "r"(taddr));
 }
 
+__device__ __forceinline__ void tmem_st8_zero(uint32_t taddr) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(taddr), "r"(0u)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
@@ -185,18 +189,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     unsigned char* base = smem_raw + (base_s - raw_s);
     const uint32_t a_s = base_s;
     const uint32_t b_s = base_s + static_cast<uint32_t>(Cfg::kOffB);
-    uint32_t* mxs = reinterpret_cast<uint32_t*>(base + Cfg::kOffMisc);            // [2][2][128]
-    uint32_t* votes = mxs + 2 * 2 * 128;                                          // [2][8]
-    int8_t* tab = reinterpret_cast<int8_t*>(votes + 2 * kConvWarps);              // 4096
+    int8_t* tab = reinterpret_cast<int8_t*>(base + Cfg::kOffMisc);                // 4096
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tab + 4096);
     // one all-ones 8x16 core matrix; with LBO = SBO = 0 it reads as a 128 x 32 all-ones A tile
     const uint32_t ones_s = smem_u32(tab + 4096 + 64);
-    uint32_t* acc_flag = tmem_slot + 1;                                           // [kBStages]
     uint64_t* a_full = reinterpret_cast<uint64_t*>(base + Cfg::kOffBar);
     uint64_t* a_empty = a_full + kAStages;
     uint64_t* b_full = a_empty + kAStages;
     uint64_t* b_empty = b_full + kBStages;
-    uint64_t* agree = b_empty + kBStages;  // [2]: converter warps published a stage's maxima/votes
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t G = gridDim.x, c = blockIdx.x;
@@ -212,13 +212,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         prefetch_tmap(&tmap);
         for (int i = 0; i < kAStages; ++i) {
             mbar_init(&a_full[i], 1);
-            mbar_init(&a_empty[i], kConvThreads / 32);
+            mbar_init(&a_empty[i], kConvWarps);
         }
         for (int i = 0; i < kBStages; ++i) {
-            mbar_init(&b_full[i], (kConvThreads + kGenThreads) / 32);
+            mbar_init(&b_full[i], kConvWarps + kGenWarps);
             mbar_init(&b_empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) mbar_init(&agree[i], kConvWarps);
         fence_barrier_init();
     }
     if (warp == 1) {
@@ -231,51 +230,49 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0) {
-        // ------------------------------ TMA producer ------------------------------
-        if (lane == 0) {
-            ChunkPos cp = chunk_pos(lo, nchunk, ntiles_col);
-            for (int it = 0; it < niter; ++it) {
-                const int sl = it % kAStages;
-                if (it >= kAStages) mbar_wait(&a_empty[sl], ((it / kAStages) - 1) & 1);
-                mbar_arrive_expect_tx(&a_full[sl], kAStageBytes);
+    if (warp < 4) {
+        // ------------------- Omega tiles (+ TMA on warp 0, MMA on warp 1) -------------------
+        // One Omega warp per SMSP (the converters' issue slots stay
+        // balanced). Warp 0's lane 0 also refills the A ring, warp 1's lane 0
+        // also issues the MMAs, one stage behind its own Omega tile.
+        constexpr int kTasksPerWarp = (2 * NPAD + 3) / 4;
+        const int task = warp * kTasksPerWarp + lane;
+        const bool has_task = lane < kTasksPerWarp && task < 2 * NPAD;
+        constexpr uint32_t kIdU = idesc_i8(NPAD, false);
+        const uint64_t ones_desc = smem_desc(ones_s, 0, 0);
+        auto issue_mma = [&](int it) {
+            const int sl = it % kBStages;
+            mbar_wait(&b_full[sl], (it / kBStages) & 1);
+            tc_fence_after();
+            const uint32_t acc = it > 0 ? 1u : 0u;  // flushed TMEM rows are zeroed by their owners
+            const uint32_t st = b_s + sl * Cfg::kBStageBytes;
+            const uint64_t bdesc = smem_desc(st + kSlices * kSliceBytes, NPAD * 16, 128);
 #pragma unroll
-                for (int b = 0; b < 2; ++b)
-                    tma_load_3d(base + sl * kAStageBytes + b * kBoxBytes, &tmap, &a_full[sl],
-                                static_cast<int>(cp.kc * kRows + 16 * b), static_cast<int>(cp.ct * kM),
-                                static_cast<int>(cp.s));
-                advance(cp, static_cast<int>(nchunk), static_cast<int>(ntiles_col));
-            }
-        }
-    } else if (warp == 1) {
-        // ------------------------------ MMA issuer ------------------------------
-        if (lane == 0) {
-            constexpr uint32_t kIdU = idesc_i8(NPAD, false);
-            const uint64_t ones_desc = smem_desc(ones_s, 0, 0);
-            for (int it = 0; it < niter; ++it) {
-                const int sl = it % kBStages;
-                mbar_wait(&b_full[sl], (it / kBStages) & 1);
-                tc_fence_after();
-                const uint32_t acc = acc_flag[sl];
-                const uint32_t st = b_s + sl * Cfg::kBStageBytes;
-                const uint64_t bdesc = smem_desc(st + kSlices * kSliceBytes, NPAD * 16, 128);
-#pragma unroll
-                for (int t = 0; t < kSlices; ++t)
-                    umma_i8(tmem + NPAD * t, smem_desc(st + t * kSliceBytes, kM * 16, 128), bdesc, kIdU, acc);
-                umma_i8(tmem + NPAD * kSlices, ones_desc, bdesc, kIdU, acc);
-                umma_commit(&b_empty[sl]);
-            }
-        }
-    } else if (warp < 4) {
-        // ------------------------------ Omega tiles ------------------------------
-        const int gt = tid - 64;  // 0..63
+            for (int t = 0; t < kSlices; ++t)
+                umma_i8(tmem + NPAD * t, smem_desc(st + t * kSliceBytes, kM * 16, 128), bdesc, kIdU, acc);
+            umma_i8(tmem + NPAD * kSlices, ones_desc, bdesc, kIdU, acc);
+            umma_commit(&b_empty[sl]);
+        };
         ChunkPos cp = chunk_pos(lo, nchunk, ntiles_col);
+        ChunkPos tp = cp;  // TMA position (warp 0)
+        auto issue_tma = [&](int it) {
+            const int sl = it % kAStages;
+            mbar_arrive_expect_tx(&a_full[sl], kAStageBytes);
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+                tma_load_3d(base + sl * kAStageBytes + b * kBoxBytes, &tmap, &a_full[sl],
+                            static_cast<int>(tp.kc * kRows + 16 * b), static_cast<int>(tp.ct * kM),
+                            static_cast<int>(tp.s));
+            advance(tp, static_cast<int>(nchunk), static_cast<int>(ntiles_col));
+        };
+        if (warp == 0 && lane == 0)
+            for (int it = 0; it < kAStages && it < niter; ++it) issue_tma(it);
         for (int it = 0; it < niter; ++it) {
             const int sl = it % kBStages;
             if (it >= kBStages) mbar_wait(&b_empty[sl], ((it / kBStages) - 1) & 1);
             const uint32_t ot = b_s + sl * Cfg::kBStageBytes + kSlices * kSliceBytes;
             const uint32_t ko = static_cast<uint32_t>((cp.kc * kRows) >> 3);
-            for (int task = gt; task < 2 * NPAD; task += kGenThreads) {
+            if (has_task) {
                 const int r = task % NPAD, h = task / NPAD;  // row, 16-byte K half
                 uint32_t w[4] = {0u, 0u, 0u, 0u};
                 if (r < p.ell) {
@@ -294,126 +291,120 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&b_full[sl]);
             advance(cp, static_cast<int>(nchunk), static_cast<int>(ntiles_col));
+            if (lane == 0) {
+                if (warp == 1 && it >= 1) issue_mma(it - 1);
+                if (warp == 0 && it + kAStages < niter) {
+                    // refill the slot the converters release after reading stage it
+                    mbar_wait(&a_empty[it % kAStages], (it / kAStages) & 1);
+                    issue_tma(it + kAStages);
+                }
+            }
+            __syncwarp();
         }
+        if (warp == 1 && lane == 0) issue_mma(niter - 1);
     } else {
         // ------------------------------ converters ------------------------------
-        // Decoupled warps: the per-stage decisions (flush? new exponents?)
-        // need every warp's overflow vote and both halves' column maxima.
-        // A warp publishes stage it+1's (agree[] mbarrier, one arrival per
-        // warp) before converting stage it, and reads it one stage later, so
-        // the agreement never phase-locks the warps: their FP64, ALU and
-        // shared-memory phases overlap.
-        const int ci = tid - 128;
-        const int half = ci >> 7, col = ci & 127;  // half 0 = warps 4..7 = TMEM lanes 0..127
-        const int cw = warp - 4;
+        // Warp 4+q owns columns [32q, 32q+32) = TMEM lanes 32q.. (the lanes it
+        // may address), all 32 rows of every stage and all slices: a column's
+        // exponent, its overflow handling and its flushes are private to one
+        // thread, and a flush only touches the warp's own D rows (read, then
+        // zeroed with tcgen05.st), so the converter warps never synchronise
+        // with each other.
+        const int q = warp - 4, col = q * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
         int eb = kEbMin, poison = 0;
         uint32_t thr = 0;
         double sclx = 0.0, scly = 1.0;
         bool tiny = false;
         int seg = 0;
-        bool first = true, pending = false;  // pending: D holds unflushed stages
+        bool first = true, pending = false;  // pending: this warp's D rows hold unflushed stages
         int psteps = 0;
         ChunkPos cp = chunk_pos(lo, nchunk, ntiles_col);
         const int nch = static_cast<int>(nchunk), ntc = static_cast<int>(ntiles_col);
 
-        // wait until the MMAs of stage `it` (and all earlier) are complete
-        auto wait_mma = [&](int it) {
-            mbar_wait(&b_empty[it % kBStages], (it / kBStages) & 1);
+        // D rows of this warp (all columns of all 8 accumulators) -> fp64
+        // partial of segment `seg` with this column's exponent; optionally
+        // zero them for the next accumulation period
+        auto flush = [&](int it_last, bool final_flush, bool zero) {
+            mbar_wait(&b_empty[it_last % kBStages], (it_last / kBStages) & 1);  // MMAs <= it_last done
             tc_fence_after();
-        };
-        // D (all columns) -> fp64 partial of segment `seg`, with this
-        // column's exponent; half 0 threads own TMEM lane `col`
-        auto flush = [&](bool final_flush) {
-            if (half == 0) {
-                double* part = p.partial + (static_cast<size_t>(c) * max_segs + seg) *
-                                               (static_cast<size_t>(NPAD) * kM);
-                const double2 u = unfix_scale(eb);
-                const uint32_t lane_base = static_cast<uint32_t>(cw * 32) << 16;
+            double* part = p.partial + (static_cast<size_t>(c) * max_segs + seg) *
+                                           (static_cast<size_t>(NPAD) * kM);
+            const double2 u = unfix_scale(eb);
 #pragma unroll 1
-                for (int g0 = 0; g0 < NPAD; g0 += 8) {
-                    // exact: sum_t 2^(8t) D_t - kOffset * D_7 as hi * 2^32 + lo
-                    long long lo64[8], hi64[8];
+            for (int g0 = 0; g0 < NPAD; g0 += 8) {
+                // exact: sum_t 2^(8t) D_t - kOffset * D_7 as hi * 2^32 + lo
+                long long lo64[8], hi64[8];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) lo64[j] = hi64[j] = 0;
+                for (int j = 0; j < 8; ++j) lo64[j] = hi64[j] = 0;
 #pragma unroll
-                    for (int t = 0; t <= kSlices; ++t) {
-                        uint32_t v[8];
-                        tmem_ld8(tmem + lane_base + NPAD * t + g0, v);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const long long d = static_cast<int>(v[j]);
-                            if (t < 4)
-                                lo64[j] += d * (1LL << (8 * t));
-                            else if (t < kSlices)
-                                hi64[j] += d * (1LL << (8 * (t - 4)));
-                            else
-                                hi64[j] -= d * kOffsetHi;
-                        }
-                    }
+                for (int t = 0; t <= kSlices; ++t) {
+                    uint32_t v[8];
+                    tmem_ld8(tmem + lane_base + NPAD * t + g0, v);
+                    tmem_ld_wait();
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        double val = fma(static_cast<double>(hi64[j]), 4294967296.0, static_cast<double>(lo64[j])) *
-                                     u.x * u.y;
-                        if (final_flush && poison) val = __longlong_as_double(0x7ff8000000000000LL);
-                        double* dst = part + static_cast<size_t>(g0 + j) * kM + col;
-                        *dst = first ? val : *dst + val;
+                        const long long d = static_cast<int>(v[j]);
+                        if (t < 4)
+                            lo64[j] += d * (1LL << (8 * t));
+                        else if (t < kSlices)
+                            hi64[j] += d * (1LL << (8 * (t - 4)));
+                        else
+                            hi64[j] -= d * kOffsetHi;
                     }
+                    if (zero) tmem_st8_zero(tmem + lane_base + NPAD * t + g0);
                 }
-                tc_fence_before();
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    double val = fma(static_cast<double>(hi64[j]), 4294967296.0, static_cast<double>(lo64[j])) *
+                                 u.x * u.y;
+                    if (final_flush && poison) val = __longlong_as_double(0x7ff8000000000000LL);
+                    double* dst = part + static_cast<size_t>(g0 + j) * kM + col;
+                    *dst = first ? val : *dst + val;
+                }
             }
+            if (zero) tmem_st_wait();
+            tc_fence_before();
             first = false;
         };
-        // stage it's 16 rows [16 half, +16) of column col: 8 conflict-free 16B loads
-        auto load = [&](int it, double (&xv)[16]) {
-            const int sa = it % kAStages;
+
+        for (int it = 0; it < niter; ++it) {
+            const int sa = it % kAStages, sb = it % kBStages;
             mbar_wait(&a_full[sa], (it / kAStages) & 1);
-            const uint32_t cb = a_s + sa * kAStageBytes + half * kBoxBytes + col * 128;
+            // rows 0..31 of column col: 16 conflict-free 16B loads (two boxes)
+            double x[32];
+            {
+                const uint32_t cb = a_s + sa * kAStageBytes + col * 128;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const double2 v = lds128(cb + ((j ^ (col & 7)) << 4));
-                xv[2 * j] = v.x;
-                xv[2 * j + 1] = v.y;
+                for (int b = 0; b < 2; ++b)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const double2 v = lds128(cb + b * kBoxBytes + ((j ^ (col & 7)) << 4));
+                        x[16 * b + 2 * j] = v.x;
+                        x[16 * b + 2 * j + 1] = v.y;
+                    }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&a_empty[sa]);
-        };
-        // publish stage it's column maximum and this warp's overflow vote
-        auto publish = [&](int it, const double (&xv)[16]) {
             uint32_t mx = 0;
 #pragma unroll
-            for (int e = 0; e < 16; ++e) mx = max(mx, static_cast<uint32_t>(__double2hiint(xv[e])) & 0x7fffffffu);
-            const int g = it & 1;
-            mxs[(g * 2 + half) * 128 + col] = mx;
-            const bool w = __any_sync(0xffffffffu, mx >= thr);
-            if (lane == 0) votes[g * kConvWarps + cw] = w ? 1u : 0u;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&agree[g]);
-        };
-
-        // one stage: decide (using the published agreement), publish the
-        // next stage, convert this one into the slice tiles
-        auto step = [&](int it, const double (&xc)[16], double (&xn)[16]) {
-            const int g = it & 1;
-            mbar_wait(&agree[g], (it >> 1) & 1);
-            bool ovf = false;
-#pragma unroll
-            for (int w = 0; w < kConvWarps; ++w) ovf = ovf || votes[g * kConvWarps + w] != 0u;
-            const uint32_t mg = max(mxs[(g * 2) * 128 + col], mxs[(g * 2 + 1) * 128 + col]);
-            const bool fresh = it == 0 || cp.kc == 0 || psteps >= kPeriodStages;
-            uint32_t accumulate = 1;
-            if (fresh || ovf) {  // CTA-uniform
-                if (pending) {   // flush the stages accumulated so far
-                    wait_mma(it - 1);
-                    flush(cp.kc == 0);  // final (poison -> NaN) if the previous stage closed its segment
+            for (int e = 0; e < 32; ++e) mx = max(mx, static_cast<uint32_t>(__double2hiint(x[e])) & 0x7fffffffu);
+            const bool new_seg = it == 0 || cp.kc == 0;
+            const bool fresh = new_seg || psteps >= kPeriodStages;
+            if (__any_sync(0xffffffffu, fresh || mx >= thr)) {  // warp-uniform, rare
+                if (pending) {
+                    // a new segment closes the old one (final: poison -> NaN);
+                    // otherwise the rows restart a period or an exponent epoch.
+                    // Either way the rows are zeroed: the MMAs always accumulate.
+                    flush(it - 1, cp.kc == 0, true);
                     if (cp.kc == 0) {
                         ++seg;
                         first = true;
                     }
                 }
-                if (it == 0 || cp.kc == 0) poison = 0;
-                if (mg >= 0x7ff00000u) poison = 1;
-                eb = column_eb(mg);
+                if (new_seg) poison = 0;
+                if (mx >= 0x7ff00000u) poison = 1;
+                eb = column_eb(mx);
                 // |x| < 2^(E+1) keeps |v| < 2^51: u = v + kOffset stays a 7-byte integer
                 thr = poison ? 0xffffffffu : (eb >= 2046 ? 0x7ff00000u : static_cast<uint32_t>(eb + 1) << 20);
                 const double2 sc2 = fix_scale(eb);
@@ -421,76 +412,64 @@ __global__ void __launch_bounds__(kThreads, 1)
                 scly = sc2.y;
                 tiny = __any_sync(0xffffffffu, scly != 1.0);
                 psteps = 0;
-                accumulate = 0;
-            }
-            if (it + 1 < niter) {
-                load(it + 1, xn);
-                publish(it + 1, xn);
-            }
-            // one DFMA per entry: t = RN(x 2^(P-E) + 1.5 2^52); its low 56 bits
-            // are u = rint(x 2^(P-E)) + kOffset (offset binary, 7 unsigned bytes)
-            uint32_t lw[16], hw[16];
-            if (!tiny) {
-#pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    const double t = fma(xc[e], sclx, kMagic);
-                    hw[e] = static_cast<uint32_t>(__double2hiint(t));
-                    lw[e] = static_cast<uint32_t>(__double2loint(t));
-                }
-            } else {
-#pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    const double t = fma(xc[e] * sclx, scly, kMagic);
-                    hw[e] = static_cast<uint32_t>(__double2hiint(t));
-                    lw[e] = static_cast<uint32_t>(__double2loint(t));
-                }
-            }
-            uint32_t sw[kSlices][4];
-#pragma unroll
-            for (int g4 = 0; g4 < 4; ++g4) {
-                const uint32_t* wl = lw + 4 * g4;
-                const uint32_t* wh = hw + 4 * g4;
-                {
-                    const uint32_t t0 = __byte_perm(wl[0], wl[1], 0x5140), t1 = __byte_perm(wl[0], wl[1], 0x7362);
-                    const uint32_t t2 = __byte_perm(wl[2], wl[3], 0x5140), t3 = __byte_perm(wl[2], wl[3], 0x7362);
-                    sw[0][g4] = __byte_perm(t0, t2, 0x5410);
-                    sw[1][g4] = __byte_perm(t0, t2, 0x7632);
-                    sw[2][g4] = __byte_perm(t1, t3, 0x5410);
-                    sw[3][g4] = __byte_perm(t1, t3, 0x7632);
-                }
-                {
-                    const uint32_t t0 = __byte_perm(wh[0], wh[1], 0x5140), t1 = __byte_perm(wh[0], wh[1], 0x7362);
-                    const uint32_t t2 = __byte_perm(wh[2], wh[3], 0x5140), t3 = __byte_perm(wh[2], wh[3], 0x7362);
-                    sw[4][g4] = __byte_perm(t0, t2, 0x5410);
-                    sw[5][g4] = __byte_perm(t0, t2, 0x7632);
-                    sw[6][g4] = __byte_perm(t1, t3, 0x5410);
-                }
             }
             // the slice slot is free once the MMAs that read it completed
-            const int sb = it % kBStages;
             if (it >= kBStages) mbar_wait(&b_empty[sb], ((it / kBStages) - 1) & 1);
-            const uint32_t st = b_s + sb * Cfg::kBStageBytes + half * (kM * 16) + col * 16;
+            // per K half (rows 16h..16h+15): one DFMA per entry -- t = RN(x 2^(P-E)
+            // + 1.5 2^52), whose low 56 bits are u = rint(x 2^(P-E)) + kOffset --
+            // then 4x4 PRMT byte transposes and one 16-byte store per slice
 #pragma unroll
-            for (int t = 0; t < kSlices; ++t) sts128u(st + t * kSliceBytes, sw[t][0], sw[t][1], sw[t][2], sw[t][3]);
-            if (ci == 0) acc_flag[sb] = accumulate;
+            for (int h = 0; h < 2; ++h) {
+                uint32_t lw[16], hw[16];
+                if (!tiny) {
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        const double t = fma(x[16 * h + e], sclx, kMagic);
+                        hw[e] = static_cast<uint32_t>(__double2hiint(t));
+                        lw[e] = static_cast<uint32_t>(__double2loint(t));
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        const double t = fma(x[16 * h + e] * sclx, scly, kMagic);
+                        hw[e] = static_cast<uint32_t>(__double2hiint(t));
+                        lw[e] = static_cast<uint32_t>(__double2loint(t));
+                    }
+                }
+                uint32_t sw[kSlices][4];
+#pragma unroll
+                for (int g4 = 0; g4 < 4; ++g4) {
+                    const uint32_t* wl = lw + 4 * g4;
+                    const uint32_t* wh = hw + 4 * g4;
+                    {
+                        const uint32_t t0 = __byte_perm(wl[0], wl[1], 0x5140), t1 = __byte_perm(wl[0], wl[1], 0x7362);
+                        const uint32_t t2 = __byte_perm(wl[2], wl[3], 0x5140), t3 = __byte_perm(wl[2], wl[3], 0x7362);
+                        sw[0][g4] = __byte_perm(t0, t2, 0x5410);
+                        sw[1][g4] = __byte_perm(t0, t2, 0x7632);
+                        sw[2][g4] = __byte_perm(t1, t3, 0x5410);
+                        sw[3][g4] = __byte_perm(t1, t3, 0x7632);
+                    }
+                    {
+                        const uint32_t t0 = __byte_perm(wh[0], wh[1], 0x5140), t1 = __byte_perm(wh[0], wh[1], 0x7362);
+                        const uint32_t t2 = __byte_perm(wh[2], wh[3], 0x5140), t3 = __byte_perm(wh[2], wh[3], 0x7362);
+                        sw[4][g4] = __byte_perm(t0, t2, 0x5410);
+                        sw[5][g4] = __byte_perm(t0, t2, 0x7632);
+                        sw[6][g4] = __byte_perm(t1, t3, 0x5410);
+                    }
+                }
+                const uint32_t st = b_s + sb * Cfg::kBStageBytes + h * (kM * 16) + col * 16;
+#pragma unroll
+                for (int t = 0; t < kSlices; ++t) sts128u(st + t * kSliceBytes, sw[t][0], sw[t][1], sw[t][2], sw[t][3]);
+            }
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) mbar_arrive(&b_full[sb]);
             pending = true;
             ++psteps;
             advance(cp, nch, ntc);
-        };
-
-        double xa[16], xb[16];
-        load(0, xa);
-        publish(0, xa);
-        for (int it = 0; it < niter; it += 2) {
-            step(it, xa, xb);
-            if (it + 1 < niter) step(it + 1, xb, xa);
         }
         // final flush of the last segment
-        wait_mma(niter - 1);
-        flush(true);
+        flush(niter - 1, true, false);
     }
     __syncthreads();
     if (warp == 1) {
