@@ -368,27 +368,36 @@ __global__ void __launch_bounds__(kThreads, 1)
             first = false;
         };
 
-        for (int it = 0; it < niter; ++it) {
-            const int sa = it % kAStages, sb = it % kBStages;
+        // rows 0..31 of column col of stage it: 16 conflict-free 16B loads (two boxes)
+        auto load = [&](int it, double (&xv)[32]) {
+            const int sa = it % kAStages;
             mbar_wait(&a_full[sa], (it / kAStages) & 1);
-            // rows 0..31 of column col: 16 conflict-free 16B loads (two boxes)
-            double x[32];
-            {
-                const uint32_t cb = a_s + sa * kAStageBytes + col * 128;
+            const uint32_t cb = a_s + sa * kAStageBytes + col * 128;
 #pragma unroll
-                for (int b = 0; b < 2; ++b)
+            for (int b = 0; b < 2; ++b)
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const double2 v = lds128(cb + b * kBoxBytes + ((j ^ (col & 7)) << 4));
-                        x[16 * b + 2 * j] = v.x;
-                        x[16 * b + 2 * j + 1] = v.y;
-                    }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&a_empty[sa]);
+                for (int j = 0; j < 8; ++j) {
+                    const double2 v = lds128(cb + b * kBoxBytes + ((j ^ (col & 7)) << 4));
+                    xv[16 * b + 2 * j] = v.x;
+                    xv[16 * b + 2 * j + 1] = v.y;
+                }
+        };
+        // max |x| high word of the stage; using it also completes the loads,
+        // so the A slot goes back to the TMA refill right after
+        auto col_max = [&](int it, const double (&xv)[32]) {
             uint32_t mx = 0;
 #pragma unroll
-            for (int e = 0; e < 32; ++e) mx = max(mx, static_cast<uint32_t>(__double2hiint(x[e])) & 0x7fffffffu);
+            for (int e = 0; e < 32; ++e) mx = max(mx, static_cast<uint32_t>(__double2hiint(xv[e])) & 0x7fffffffu);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&a_empty[it % kAStages]);
+            return mx;
+        };
+
+        // stage it (entries xc, column max mx): exponent bookkeeping, then
+        // the next stage's loads are issued and this stage is converted while
+        // they are in flight
+        auto step = [&](int it, const double (&xc)[32], uint32_t mx, double (&xn)[32]) -> uint32_t {
+            const int sb = it % kBStages;
             const bool new_seg = it == 0 || cp.kc == 0;
             const bool fresh = new_seg || psteps >= kPeriodStages;
             if (__any_sync(0xffffffffu, fresh || mx >= thr)) {  // warp-uniform, rare
@@ -413,6 +422,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tiny = __any_sync(0xffffffffu, scly != 1.0);
                 psteps = 0;
             }
+            const bool more = it + 1 < niter;
+            if (more) load(it + 1, xn);
             // the slice slot is free once the MMAs that read it completed
             if (it >= kBStages) mbar_wait(&b_empty[sb], ((it / kBStages) - 1) & 1);
             // per K half (rows 16h..16h+15): one DFMA per entry -- t = RN(x 2^(P-E)
@@ -424,14 +435,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (!tiny) {
 #pragma unroll
                     for (int e = 0; e < 16; ++e) {
-                        const double t = fma(x[16 * h + e], sclx, kMagic);
+                        const double t = fma(xc[16 * h + e], sclx, kMagic);
                         hw[e] = static_cast<uint32_t>(__double2hiint(t));
                         lw[e] = static_cast<uint32_t>(__double2loint(t));
                     }
                 } else {
 #pragma unroll
                     for (int e = 0; e < 16; ++e) {
-                        const double t = fma(x[16 * h + e] * sclx, scly, kMagic);
+                        const double t = fma(xc[16 * h + e] * sclx, scly, kMagic);
                         hw[e] = static_cast<uint32_t>(__double2hiint(t));
                         lw[e] = static_cast<uint32_t>(__double2loint(t));
                     }
@@ -467,6 +478,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             pending = true;
             ++psteps;
             advance(cp, nch, ntc);
+            return more ? col_max(it + 1, xn) : 0u;
+        };
+
+        double xa[32], xb[32];
+        load(0, xa);
+        uint32_t mx = col_max(0, xa);
+        for (int it = 0; it < niter; it += 2) {
+            mx = step(it, xa, mx, xb);
+            if (it + 1 < niter) mx = step(it + 1, xb, mx, xa);
         }
         // final flush of the last segment
         flush(niter - 1, true, false);
