@@ -21,20 +21,20 @@
 // columns [N t, N t + N)) += slice_t(A^T) (128 x 32, K-major) *
 // Q^T (32 x N, K-major), one MMA per slice per 32-row stage.
 //
-// Warp roles (256 threads, persistent, one CTA per SM, stream-K over
+// Warp roles (384 threads, persistent, one CTA per SM, stream-K over
 // (subdomain, 128-column tile, 32-row stage) like sketch.cu):
 //   warps 0-3   Omega: Philox + quantile table -> K-major int8 tile, one
 //               warp per SMSP; warp 0's lane 0 also keeps the A ring full
 //               (two 16x128 fp64 TMA boxes, 128B swizzle, per stage), warp
 //               1 allocates TMEM and its lane 0 issues the 8 MMAs per stage
 //               (one stage behind), committed to the slot's "empty" mbarrier
-//   warps 4-7   converters, one per TMEM lane quarter; thread = column c:
-//               its 32 fp64 entries of the stage -> one DFMA each (offset-
-//               binary fixed point, below) -> 4x4 PRMT byte transposes ->
-//               one 16-byte store per slice and K half into the K-major
-//               slice tiles. The thread owns D row c: its rare flushes read
-//               the row (tcgen05.ld 32x32b) into the fp64 partial and zero
-//               it (tcgen05.st), without involving any other warp.
+//   warps 4-11  converters, two per TMEM lane quarter, 16 columns each;
+//               thread = (column, row half): 16 fp64 entries of the stage ->
+//               one DFMA each (offset-binary fixed point, below) -> 4x4 PRMT
+//               byte transposes -> one 16-byte store per slice into the
+//               K-major slice tile. A warp owns its 16 D rows: its rare
+//               flushes read them (tcgen05.ld 16x64b) into the fp64 partial
+//               and zero them (tcgen05.st), without involving another warp.
 // A warp flushes its rows at segment ends, every 2048 stages (|D| < 2^31)
 // and when one of its columns exceeds its exponent headroom.
 #include <math.h>
@@ -47,8 +47,8 @@ namespace spidgpu {
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kConvWarps = 4;         // warps 4..7: one per TMEM lane quarter
+constexpr int kThreads = 384;
+constexpr int kConvWarps = 8;         // warps 4..11: two per TMEM lane quarter
 constexpr int kGenWarps = 4;          // warps 0..3 (one per SMSP)
 constexpr int kM = 128;               // snapshots per CTA tile (UMMA M)
 constexpr int kRows = 32;             // rows of A per stage (UMMA K for int8)
@@ -148,6 +148,18 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
                  : "r"(taddr));
 }
 
+// .16x64b: the warp's 16 lanes from the address' lane field; thread t holds
+// lane 8 (t & 1) + (t >> 2), columns ((t >> 1) & 1) + 2 j (probed on B200:
+// tools/microbench/tmem_16dp.cu)
+__device__ __forceinline__ void tmem_ld16x64b_x8(uint32_t taddr, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.16x64b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16x64b_x8_zero(uint32_t taddr) {
+    asm volatile("tcgen05.st.sync.aligned.16x64b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(taddr), "r"(0u)
+                 : "memory");
+}
 __device__ __forceinline__ void tmem_st8_zero(uint32_t taddr) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(taddr), "r"(0u)
                  : "memory");
@@ -215,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&a_empty[i], kConvWarps);
         }
         for (int i = 0; i < kBStages; ++i) {
-            mbar_init(&b_full[i], kConvWarps + kGenWarps);
+            mbar_init(&b_full[i], kConvWarps + kGenWarps - 1);
             mbar_init(&b_empty[i], 1);
         }
         fence_barrier_init();
@@ -232,12 +244,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp < 4) {
         // ------------------- Omega tiles (+ TMA on warp 0, MMA on warp 1) -------------------
-        // One Omega warp per SMSP (the converters' issue slots stay
-        // balanced). Warp 0's lane 0 also refills the A ring, warp 1's lane 0
-        // also issues the MMAs, one stage behind its own Omega tile.
-        constexpr int kTasksPerWarp = (2 * NPAD + 3) / 4;
-        const int task = warp * kTasksPerWarp + lane;
-        const bool has_task = lane < kTasksPerWarp && task < 2 * NPAD;
+        // Warps 0, 2, 3 generate the Omega tile (warp 0's lane 0 also refills
+        // the A ring); warp 1's lane 0 only issues the MMAs, as soon as a
+        // stage's slices and Omega are complete.
+        constexpr int kTasksPerWarp = (2 * NPAD + 2) / 3;  // warps 0, 2, 3 share the Omega tile
+        const int gw = warp == 0 ? 0 : warp - 1;
+
         constexpr uint32_t kIdU = idesc_i8(NPAD, false);
         const uint64_t ones_desc = smem_desc(ones_s, 0, 0);
         auto issue_mma = [&](int it) {
@@ -267,12 +279,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         if (warp == 0 && lane == 0)
             for (int it = 0; it < kAStages && it < niter; ++it) issue_tma(it);
+        if (warp == 1) {  // dedicated MMA issuer: no Omega work, so MMAs go out as soon as a stage is full
+            if (lane == 0)
+                for (int it = 0; it < niter; ++it) issue_mma(it);
+        } else
         for (int it = 0; it < niter; ++it) {
             const int sl = it % kBStages;
             if (it >= kBStages) mbar_wait(&b_empty[sl], ((it / kBStages) - 1) & 1);
             const uint32_t ot = b_s + sl * Cfg::kBStageBytes + kSlices * kSliceBytes;
             const uint32_t ko = static_cast<uint32_t>((cp.kc * kRows) >> 3);
-            if (has_task) {
+            for (int tk = lane; tk < kTasksPerWarp; tk += 32) {
+                const int task = gw * kTasksPerWarp + tk;
+                if (task >= 2 * NPAD) break;
                 const int r = task % NPAD, h = task / NPAD;  // row, 16-byte K half
                 uint32_t w[4] = {0u, 0u, 0u, 0u};
                 if (r < p.ell) {
@@ -292,7 +310,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) mbar_arrive(&b_full[sl]);
             advance(cp, static_cast<int>(nchunk), static_cast<int>(ntiles_col));
             if (lane == 0) {
-                if (warp == 1 && it >= 1) issue_mma(it - 1);
                 if (warp == 0 && it + kAStages < niter) {
                     // refill the slot the converters release after reading stage it
                     mbar_wait(&a_empty[it % kAStages], (it / kAStages) & 1);
@@ -301,17 +318,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             __syncwarp();
         }
-        if (warp == 1 && lane == 0) issue_mma(niter - 1);
     } else {
         // ------------------------------ converters ------------------------------
-        // Warp 4+q owns columns [32q, 32q+32) = TMEM lanes 32q.. (the lanes it
-        // may address), all 32 rows of every stage and all slices: a column's
-        // exponent, its overflow handling and its flushes are private to one
-        // thread, and a flush only touches the warp's own D rows (read, then
-        // zeroed with tcgen05.st), so the converter warps never synchronise
-        // with each other.
-        const int q = warp - 4, col = q * 32 + lane;
-        const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+        // Two warps per TMEM lane quarter: warp w (4..11) owns the 16 columns
+        // 32 (w % 4) + 16 hh + [0, 16) (hh = (w - 4) / 4) = those TMEM lanes,
+        // all 32 rows of every stage and all slices. Conversion: lane =
+        // (column cc = lane & 15, row half b = lane >> 4), 16 entries each;
+        // the two halves of a column share its exponent through one shuffle.
+        // Flush: tcgen05.ld/st .16x64b touch only the warp's 16 lanes (lane L
+        // = 8 (t & 1) + (t >> 2), column parity (t >> 1) & 1 per thread t), so
+        // a column's overflow handling and flushes never involve another warp.
+        const int q = warp & 3, hh = (warp - 4) >> 2;
+        const int cc = lane & 15, b = lane >> 4;
+        const int col = q * 32 + hh * 16 + cc;
+        const uint32_t lane_base = static_cast<uint32_t>(q * 32 + hh * 16) << 16;
+        const int lf = 8 * (lane & 1) + (lane >> 2), pf = (lane >> 1) & 1;  // flush: D lane, column parity
+        const int col_f = q * 32 + hh * 16 + lf;
         int eb = kEbMin, poison = 0;
         uint32_t thr = 0;
         double sclx = 0.0, scly = 1.0;
@@ -323,24 +345,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int nch = static_cast<int>(nchunk), ntc = static_cast<int>(ntiles_col);
 
         // D rows of this warp (all columns of all 8 accumulators) -> fp64
-        // partial of segment `seg` with this column's exponent; optionally
-        // zero them for the next accumulation period
+        // partial of segment `seg` with each row's exponent; optionally zero
+        // them for the next accumulation period
         auto flush = [&](int it_last, bool final_flush, bool zero) {
             mbar_wait(&b_empty[it_last % kBStages], (it_last / kBStages) & 1);  // MMAs <= it_last done
             tc_fence_after();
             double* part = p.partial + (static_cast<size_t>(c) * max_segs + seg) *
                                            (static_cast<size_t>(NPAD) * kM);
-            const double2 u = unfix_scale(eb);
+            const int ebf = __shfl_sync(0xffffffffu, eb, lf);       // lane lf converts column lf (b = 0)
+            const int psf = __shfl_sync(0xffffffffu, poison, lf);
+            const double2 u = unfix_scale(ebf);
 #pragma unroll 1
-            for (int g0 = 0; g0 < NPAD; g0 += 8) {
-                // exact: sum_t 2^(8t) D_t - kOffset * D_7 as hi * 2^32 + lo
+            for (int g0 = 0; g0 < NPAD; g0 += 16) {
+                // exact: sum_t 2^(8t) D_t - kOffset * D_7 as hi * 2^32 + lo, for
+                // columns g0 + pf + 2j of D row lf
                 long long lo64[8], hi64[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) lo64[j] = hi64[j] = 0;
 #pragma unroll
                 for (int t = 0; t <= kSlices; ++t) {
                     uint32_t v[8];
-                    tmem_ld8(tmem + lane_base + NPAD * t + g0, v);
+                    tmem_ld16x64b_x8(tmem + lane_base + NPAD * t + g0, v);
                     tmem_ld_wait();
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
@@ -352,14 +377,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         else
                             hi64[j] -= d * kOffsetHi;
                     }
-                    if (zero) tmem_st8_zero(tmem + lane_base + NPAD * t + g0);
+                    if (zero) tmem_st16x64b_x8_zero(tmem + lane_base + NPAD * t + g0);
                 }
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     double val = fma(static_cast<double>(hi64[j]), 4294967296.0, static_cast<double>(lo64[j])) *
                                  u.x * u.y;
-                    if (final_flush && poison) val = __longlong_as_double(0x7ff8000000000000LL);
-                    double* dst = part + static_cast<size_t>(g0 + j) * kM + col;
+                    if (final_flush && psf) val = __longlong_as_double(0x7ff8000000000000LL);
+                    double* dst = part + static_cast<size_t>(g0 + pf + 2 * j) * kM + col_f;
                     *dst = first ? val : *dst + val;
                 }
             }
@@ -368,35 +393,31 @@ __global__ void __launch_bounds__(kThreads, 1)
             first = false;
         };
 
-        // rows 0..31 of column col of stage it: 16 conflict-free 16B loads (two boxes)
-        auto load = [&](int it, double (&xv)[32]) {
+        // rows [16 b, 16 b + 16) of column col of stage it: 8 conflict-free 16B loads
+        auto load = [&](int it, double (&xv)[16]) {
             const int sa = it % kAStages;
             mbar_wait(&a_full[sa], (it / kAStages) & 1);
-            const uint32_t cb = a_s + sa * kAStageBytes + col * 128;
+            const uint32_t cb = a_s + sa * kAStageBytes + b * kBoxBytes + col * 128;
 #pragma unroll
-            for (int b = 0; b < 2; ++b)
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const double2 v = lds128(cb + b * kBoxBytes + ((j ^ (col & 7)) << 4));
-                    xv[16 * b + 2 * j] = v.x;
-                    xv[16 * b + 2 * j + 1] = v.y;
-                }
+            for (int j = 0; j < 8; ++j) {
+                const double2 v = lds128(cb + ((j ^ (col & 7)) << 4));
+                xv[2 * j] = v.x;
+                xv[2 * j + 1] = v.y;
+            }
         };
-        // max |x| high word of the stage; using it also completes the loads,
-        // so the A slot goes back to the TMA refill right after
-        auto col_max = [&](int it, const double (&xv)[32]) {
+        // column max |x| high word over both row halves; using it also
+        // completes the loads, so the A slot goes back to the TMA refill
+        auto col_max = [&](int it, const double (&xv)[16]) {
             uint32_t mx = 0;
 #pragma unroll
-            for (int e = 0; e < 32; ++e) mx = max(mx, static_cast<uint32_t>(__double2hiint(xv[e])) & 0x7fffffffu);
+            for (int e = 0; e < 16; ++e) mx = max(mx, static_cast<uint32_t>(__double2hiint(xv[e])) & 0x7fffffffu);
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
             __syncwarp();
             if (lane == 0) mbar_arrive(&a_empty[it % kAStages]);
             return mx;
         };
 
-        // stage it (entries xc, column max mx): exponent bookkeeping, then
-        // the next stage's loads are issued and this stage is converted while
-        // they are in flight
-        auto step = [&](int it, const double (&xc)[32], uint32_t mx, double (&xn)[32]) -> uint32_t {
+        auto step = [&](int it, const double (&xc)[16], uint32_t mx, double (&xn)[16]) -> uint32_t {
             const int sb = it % kBStages;
             const bool new_seg = it == 0 || cp.kc == 0;
             const bool fresh = new_seg || psteps >= kPeriodStages;
@@ -426,52 +447,49 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (more) load(it + 1, xn);
             // the slice slot is free once the MMAs that read it completed
             if (it >= kBStages) mbar_wait(&b_empty[sb], ((it / kBStages) - 1) & 1);
-            // per K half (rows 16h..16h+15): one DFMA per entry -- t = RN(x 2^(P-E)
-            // + 1.5 2^52), whose low 56 bits are u = rint(x 2^(P-E)) + kOffset --
-            // then 4x4 PRMT byte transposes and one 16-byte store per slice
+            // one DFMA per entry -- t = RN(x 2^(P-E) + 1.5 2^52), whose low 56
+            // bits are u = rint(x 2^(P-E)) + kOffset -- then 4x4 PRMT byte
+            // transposes and one 16-byte store per slice (K half b, row col)
+            uint32_t lw[16], hw[16];
+            if (!tiny) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                uint32_t lw[16], hw[16];
-                if (!tiny) {
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const double t = fma(xc[16 * h + e], sclx, kMagic);
-                        hw[e] = static_cast<uint32_t>(__double2hiint(t));
-                        lw[e] = static_cast<uint32_t>(__double2loint(t));
-                    }
-                } else {
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const double t = fma(xc[16 * h + e] * sclx, scly, kMagic);
-                        hw[e] = static_cast<uint32_t>(__double2hiint(t));
-                        lw[e] = static_cast<uint32_t>(__double2loint(t));
-                    }
+                for (int e = 0; e < 16; ++e) {
+                    const double t = fma(xc[e], sclx, kMagic);
+                    hw[e] = static_cast<uint32_t>(__double2hiint(t));
+                    lw[e] = static_cast<uint32_t>(__double2loint(t));
                 }
-                uint32_t sw[kSlices][4];
+            } else {
 #pragma unroll
-                for (int g4 = 0; g4 < 4; ++g4) {
-                    const uint32_t* wl = lw + 4 * g4;
-                    const uint32_t* wh = hw + 4 * g4;
-                    {
-                        const uint32_t t0 = __byte_perm(wl[0], wl[1], 0x5140), t1 = __byte_perm(wl[0], wl[1], 0x7362);
-                        const uint32_t t2 = __byte_perm(wl[2], wl[3], 0x5140), t3 = __byte_perm(wl[2], wl[3], 0x7362);
-                        sw[0][g4] = __byte_perm(t0, t2, 0x5410);
-                        sw[1][g4] = __byte_perm(t0, t2, 0x7632);
-                        sw[2][g4] = __byte_perm(t1, t3, 0x5410);
-                        sw[3][g4] = __byte_perm(t1, t3, 0x7632);
-                    }
-                    {
-                        const uint32_t t0 = __byte_perm(wh[0], wh[1], 0x5140), t1 = __byte_perm(wh[0], wh[1], 0x7362);
-                        const uint32_t t2 = __byte_perm(wh[2], wh[3], 0x5140), t3 = __byte_perm(wh[2], wh[3], 0x7362);
-                        sw[4][g4] = __byte_perm(t0, t2, 0x5410);
-                        sw[5][g4] = __byte_perm(t0, t2, 0x7632);
-                        sw[6][g4] = __byte_perm(t1, t3, 0x5410);
-                    }
+                for (int e = 0; e < 16; ++e) {
+                    const double t = fma(xc[e] * sclx, scly, kMagic);
+                    hw[e] = static_cast<uint32_t>(__double2hiint(t));
+                    lw[e] = static_cast<uint32_t>(__double2loint(t));
                 }
-                const uint32_t st = b_s + sb * Cfg::kBStageBytes + h * (kM * 16) + col * 16;
-#pragma unroll
-                for (int t = 0; t < kSlices; ++t) sts128u(st + t * kSliceBytes, sw[t][0], sw[t][1], sw[t][2], sw[t][3]);
             }
+            uint32_t sw[kSlices][4];
+#pragma unroll
+            for (int g4 = 0; g4 < 4; ++g4) {
+                const uint32_t* wl = lw + 4 * g4;
+                const uint32_t* wh = hw + 4 * g4;
+                {
+                    const uint32_t t0 = __byte_perm(wl[0], wl[1], 0x5140), t1 = __byte_perm(wl[0], wl[1], 0x7362);
+                    const uint32_t t2 = __byte_perm(wl[2], wl[3], 0x5140), t3 = __byte_perm(wl[2], wl[3], 0x7362);
+                    sw[0][g4] = __byte_perm(t0, t2, 0x5410);
+                    sw[1][g4] = __byte_perm(t0, t2, 0x7632);
+                    sw[2][g4] = __byte_perm(t1, t3, 0x5410);
+                    sw[3][g4] = __byte_perm(t1, t3, 0x7632);
+                }
+                {
+                    const uint32_t t0 = __byte_perm(wh[0], wh[1], 0x5140), t1 = __byte_perm(wh[0], wh[1], 0x7362);
+                    const uint32_t t2 = __byte_perm(wh[2], wh[3], 0x5140), t3 = __byte_perm(wh[2], wh[3], 0x7362);
+                    sw[4][g4] = __byte_perm(t0, t2, 0x5410);
+                    sw[5][g4] = __byte_perm(t0, t2, 0x7632);
+                    sw[6][g4] = __byte_perm(t1, t3, 0x5410);
+                }
+            }
+            const uint32_t st = b_s + sb * Cfg::kBStageBytes + b * (kM * 16) + col * 16;
+#pragma unroll
+            for (int t = 0; t < kSlices; ++t) sts128u(st + t * kSliceBytes, sw[t][0], sw[t][1], sw[t][2], sw[t][3]);
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) mbar_arrive(&b_full[sb]);
@@ -481,7 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             return more ? col_max(it + 1, xn) : 0u;
         };
 
-        double xa[32], xb[32];
+        double xa[16], xb[16];
         load(0, xa);
         uint32_t mx = col_max(0, xa);
         for (int it = 0; it < niter; it += 2) {
