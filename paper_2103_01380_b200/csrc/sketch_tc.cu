@@ -65,9 +65,9 @@ constexpr int kEbMin = 9;
 constexpr int kPeriodStages = 2048;   // 65536 rows: 65536 * 117 * 255 < 2^31
 constexpr int kBoxBytes = 16 * kM * 8;              // 16 rows x 128 columns fp64
 constexpr int kAStageBytes = 2 * kBoxBytes;         // 32 KB
-constexpr int kAStages = 4;
+constexpr int kAStages = 5;
 constexpr int kSliceBytes = kM * kRows;             // 4 KB per slice tile
-constexpr int kBStages = 3;
+constexpr int kBStages = 2;
 
 template <int NPAD>
 struct TcCfg {
