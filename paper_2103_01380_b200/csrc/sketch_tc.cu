@@ -39,6 +39,8 @@
 // and when one of its columns exceeds its exponent headroom.
 #include <math.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "philox.cuh"
@@ -449,47 +451,47 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (it >= kBStages) mbar_wait(&b_empty[sb], ((it / kBStages) - 1) & 1);
             // one DFMA per entry -- t = RN(x 2^(P-E) + 1.5 2^52), whose low 56
             // bits are u = rint(x 2^(P-E)) + kOffset -- then 4x4 PRMT byte
-            // transposes and one 16-byte store per slice (K half b, row col)
-            uint32_t lw[16], hw[16];
-            if (!tiny) {
-#pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    const double t = fma(xc[e], sclx, kMagic);
-                    hw[e] = static_cast<uint32_t>(__double2hiint(t));
-                    lw[e] = static_cast<uint32_t>(__double2loint(t));
-                }
-            } else {
-#pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    const double t = fma(xc[e] * sclx, scly, kMagic);
-                    hw[e] = static_cast<uint32_t>(__double2hiint(t));
-                    lw[e] = static_cast<uint32_t>(__double2loint(t));
-                }
-            }
-            uint32_t sw[kSlices][4];
-#pragma unroll
-            for (int g4 = 0; g4 < 4; ++g4) {
-                const uint32_t* wl = lw + 4 * g4;
-                const uint32_t* wh = hw + 4 * g4;
-                {
-                    const uint32_t t0 = __byte_perm(wl[0], wl[1], 0x5140), t1 = __byte_perm(wl[0], wl[1], 0x7362);
-                    const uint32_t t2 = __byte_perm(wl[2], wl[3], 0x5140), t3 = __byte_perm(wl[2], wl[3], 0x7362);
-                    sw[0][g4] = __byte_perm(t0, t2, 0x5410);
-                    sw[1][g4] = __byte_perm(t0, t2, 0x7632);
-                    sw[2][g4] = __byte_perm(t1, t3, 0x5410);
-                    sw[3][g4] = __byte_perm(t1, t3, 0x7632);
-                }
-                {
-                    const uint32_t t0 = __byte_perm(wh[0], wh[1], 0x5140), t1 = __byte_perm(wh[0], wh[1], 0x7362);
-                    const uint32_t t2 = __byte_perm(wh[2], wh[3], 0x5140), t3 = __byte_perm(wh[2], wh[3], 0x7362);
-                    sw[4][g4] = __byte_perm(t0, t2, 0x5410);
-                    sw[5][g4] = __byte_perm(t0, t2, 0x7632);
-                    sw[6][g4] = __byte_perm(t1, t3, 0x5410);
-                }
-            }
+            // transposes and one 16-byte store per slice (K half b, row col).
+            // The rare two-factor scale (tiny columns) is a separate copy of
+            // the whole emit path, so the hot path has no register joins.
             const uint32_t st = b_s + sb * Cfg::kBStageBytes + b * (kM * 16) + col * 16;
+            auto emit = [&](auto two_factor) {
+                uint32_t lw[16], hw[16];
 #pragma unroll
-            for (int t = 0; t < kSlices; ++t) sts128u(st + t * kSliceBytes, sw[t][0], sw[t][1], sw[t][2], sw[t][3]);
+                for (int e = 0; e < 16; ++e) {
+                    const double t = decltype(two_factor)::value ? fma(xc[e] * sclx, scly, kMagic)
+                                                                 : fma(xc[e], sclx, kMagic);
+                    hw[e] = static_cast<uint32_t>(__double2hiint(t));
+                    lw[e] = static_cast<uint32_t>(__double2loint(t));
+                }
+                uint32_t sw[kSlices][4];
+#pragma unroll
+                for (int g4 = 0; g4 < 4; ++g4) {
+                    const uint32_t* wl = lw + 4 * g4;
+                    const uint32_t* wh = hw + 4 * g4;
+                    {
+                        const uint32_t t0 = __byte_perm(wl[0], wl[1], 0x5140), t1 = __byte_perm(wl[0], wl[1], 0x7362);
+                        const uint32_t t2 = __byte_perm(wl[2], wl[3], 0x5140), t3 = __byte_perm(wl[2], wl[3], 0x7362);
+                        sw[0][g4] = __byte_perm(t0, t2, 0x5410);
+                        sw[1][g4] = __byte_perm(t0, t2, 0x7632);
+                        sw[2][g4] = __byte_perm(t1, t3, 0x5410);
+                        sw[3][g4] = __byte_perm(t1, t3, 0x7632);
+                    }
+                    {
+                        const uint32_t t0 = __byte_perm(wh[0], wh[1], 0x5140), t1 = __byte_perm(wh[0], wh[1], 0x7362);
+                        const uint32_t t2 = __byte_perm(wh[2], wh[3], 0x5140), t3 = __byte_perm(wh[2], wh[3], 0x7362);
+                        sw[4][g4] = __byte_perm(t0, t2, 0x5410);
+                        sw[5][g4] = __byte_perm(t0, t2, 0x7632);
+                        sw[6][g4] = __byte_perm(t1, t3, 0x5410);
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < kSlices; ++t) sts128u(st + t * kSliceBytes, sw[t][0], sw[t][1], sw[t][2], sw[t][3]);
+            };
+            if (!tiny)
+                emit(std::false_type{});
+            else
+                emit(std::true_type{});
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) mbar_arrive(&b_full[sb]);
