@@ -493,24 +493,42 @@ def quality_spid(eng, cfg, field, A, first, count, world, stream):
 
 def e2e_measure(eng, cfg, A, first, count, rule, args, world):
     """The same metric through the C-ABI host call (spidgpu_compress_host):
-    pinned host A in, host factors out, every copy inside the timed region."""
+    pinned host A in, host factors out, every copy inside the timed region.
+
+    The pinned sample is sized to the host: at most 40% of the available
+    host memory is pinned across all local ranks (8 ranks x 64 subdomains
+    would pin ~190 GB); the ranks agree on success before any collective."""
+    import psutil
     import torch
     import torch.distributed as dist
 
-    a_host = torch.empty(A.shape, dtype=torch.float64, pin_memory=True)
-    a_host.copy_(A)
     kcap = rule.cap(cfg.ell, cfg.n)
-    out = {
-        "indices": torch.empty((count, kcap), dtype=torch.int64, pin_memory=True),
-        "coeffs": torch.empty((count, cfg.n, kcap), dtype=torch.float64, pin_memory=True),
-        "skel": torch.empty((count, kcap, cfg.m), dtype=torch.float64, pin_memory=True),
-        "rank": torch.empty(count, dtype=torch.int64, pin_memory=True),
-        "residual_fro": torch.empty(count, dtype=torch.float64, pin_memory=True),
-        "status": torch.empty(count, dtype=torch.int32, pin_memory=True),
-    }
-    eng.compress_host(a_host, cfg.ell, rule, seed=cfg.seed, subdomain_base=first, group=8,
-                      out=out)  # warm-up (allocates the lane buffers)
-    torch.cuda.synchronize()
+    per_sub = (cfg.m * cfg.n + cfg.m * kcap + cfg.n * kcap) * 8
+    avail = psutil.virtual_memory().available
+    local_ranks = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    ne = int(min(count, max(1, (0.4 * avail) // (local_ranks * per_sub))))
+    ok, err = 1, ""
+    try:
+        a_host = torch.empty((ne,) + tuple(A.shape[1:]), dtype=torch.float64, pin_memory=True)
+        a_host.copy_(A[:ne])
+        out = {
+            "indices": torch.empty((ne, kcap), dtype=torch.int64, pin_memory=True),
+            "coeffs": torch.empty((ne, cfg.n, kcap), dtype=torch.float64, pin_memory=True),
+            "skel": torch.empty((ne, kcap, cfg.m), dtype=torch.float64, pin_memory=True),
+            "rank": torch.empty(ne, dtype=torch.int64, pin_memory=True),
+            "residual_fro": torch.empty(ne, dtype=torch.float64, pin_memory=True),
+            "status": torch.empty(ne, dtype=torch.int32, pin_memory=True),
+        }
+        eng.compress_host(a_host, cfg.ell, rule, seed=cfg.seed, subdomain_base=first, group=8,
+                          out=out)  # warm-up (allocates the lane buffers)
+        torch.cuda.synchronize()
+    except Exception as e:  # host memory / pinning failure: reported, never fatal
+        ok, err = 0, repr(e)
+    flag = torch.tensor([ok], dtype=torch.int32, device=eng.dev)
+    if world > 1:
+        _allreduce(flag, op=dist.ReduceOp.MIN)
+    if not int(flag[0]):
+        return {"error": err or "another rank could not pin its e2e sample"}
     if world > 1:
         dist.barrier()
     t = time.perf_counter()
@@ -524,10 +542,10 @@ def e2e_measure(eng, cfg, A, first, count, rule, args, world):
     sec = float(el[0])
     h2d = a_host.numel() * 8
     d2h = sum(v.numel() * v.element_size() for v in out.values())
-    return {"value": cfg.raw_bytes(count) * world / sec / 1e9, "unit": "GB/s",
+    return {"value": cfg.raw_bytes(ne) * world / sec / 1e9, "unit": "GB/s",
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "api": "spidgpu_compress_host (C ABI, pinned host buffers, 2 copy/compute lanes)",
-            "steps": args.e2e_steps, "ms_per_step": sec * 1e3}
+            "subdomains_per_rank": ne, "steps": args.e2e_steps, "ms_per_step": sec * 1e3}
 
 
 def global_field(A, grid, block, qoi):
