@@ -377,7 +377,8 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {count} subdomains/GPU of 32^3 x 5 QoIs x "
                                f"{cfg.n} snapshots ({cfg.m}x{cfg.n} fp64), k={cfg.k}, p={cfg.p}, "
-                               f"Philox Omega; global blocks [{first}, {first + count}) per rank of "
+                               f"in-kernel Philox Omega (discretised Gaussian Q/32); global blocks "
+                               f"[64r, 64r+64) on rank r (rank 0: [{first}, {first + count})) of "
                                f"the {field.grid}^3 multimode TGV field",
                    "global_batch": count * world, "seq_len": cfg.n, "parallelism": f"dp{world}",
                    "l2": "inputs (21.5 GB/GPU) larger than L2 (126 MB); no flush needed"},

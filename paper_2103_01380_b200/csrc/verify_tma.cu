@@ -22,6 +22,8 @@
 //  * err/ref are summed per lane, reduced per warp, written per (CTA, tile
 //    segment, warp) and summed in a fixed order by a second kernel, so the
 //    result is bitwise reproducible run to run.
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -136,20 +138,29 @@ __global__ void __launch_bounds__(kThreadsV, 1)
         for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
             for (int nt = 0; nt < NWV; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+        // full-rank tiles (the common case) take a branch-free DMMA burst;
+        // partial ranks mask the skeleton columns >= rank (their contents
+        // are not part of the factor and may be anything, even NaN)
+        auto kloop = [&](auto full) {
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-            if (ks < ksteps) {
-                const int t = 4 * ks + q4;
-                // skeleton rows 2*grow, 2*grow+1 of column t (16B chunk grow, swizzled by t%8)
-                double2 sv = lds128(st + t * 128 + ((grow ^ (t & 7)) << 4));
-                if (t >= rank) sv.x = sv.y = 0.0;  // columns >= rank are not part of the factor
+            for (int ks = 0; ks < KS; ++ks) {
+                if (decltype(full)::value || ks < ksteps) {
+                    const int t = 4 * ks + q4;
+                    // skeleton rows 2*grow, 2*grow+1 of column t (16B chunk grow, swizzled by t%8)
+                    double2 sv = lds128(st + t * 128 + ((grow ^ (t & 7)) << 4));
+                    if (!decltype(full)::value && t >= rank) sv.x = sv.y = 0.0;
 #pragma unroll
-                for (int nt = 0; nt < NWV; ++nt) {
-                    dmma(acc[0][nt][0], acc[0][nt][1], sv.x, cfr[ks][nt]);
-                    dmma(acc[1][nt][0], acc[1][nt][1], sv.y, cfr[ks][nt]);
+                    for (int nt = 0; nt < NWV; ++nt) {
+                        dmma(acc[0][nt][0], acc[0][nt][1], sv.x, cfr[ks][nt]);
+                        dmma(acc[1][nt][0], acc[1][nt][1], sv.y, cfr[ks][nt]);
+                    }
                 }
             }
-        }
+        };
+        if (rank == 4 * KS)
+            kloop(std::true_type{});
+        else
+            kloop(std::false_type{});
         // compare with A: accumulator (mt, nt, e) is row 2*grow+mt, column col0+8nt+2q4+e
 #pragma unroll
         for (int nt = 0; nt < NWV; ++nt)
