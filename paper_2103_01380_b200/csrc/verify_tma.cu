@@ -14,7 +14,7 @@
 //  * 1 producer warp issues two TMA boxes per chunk -- A (16 rows x NT
 //    columns) and the skeleton rows (16 rows x 4*KS columns), both 128B
 //    swizzled -- into an S-stage mbarrier ring;
-//  * 16 consumer warps; warp w owns columns [8*NWV*w, 8*NWV*(w+1)) of the
+//  * 8 consumer warps; warp w owns columns [8*NWV*w, 8*NWV*(w+1)) of the
 //    tile and keeps C's fragments for them in registers for the whole tile;
 //    accumulator row (mt, grow) is chunk row 2*grow + mt, so one 16-byte
 //    shared load yields both M tiles' skeleton fragment, and one yields the
@@ -32,7 +32,7 @@ namespace spidgpu {
 namespace {
 
 constexpr int kRows = 16;          // rows per chunk (one 128 B swizzle row)
-constexpr int kCons = 16;          // consumer warps
+constexpr int kCons = 8;           // consumer warps (2 per SMSP: 170 registers each)
 constexpr int kThreadsV = (kCons + 1) * kWarp;
 constexpr int kBudget = 200 * 1024;
 
@@ -251,13 +251,22 @@ cudaError_t launch_t(const VerifyParams& p, const VerifyPlan& plan, const CUtens
 template <int NWV>
 cudaError_t launch_ks(const VerifyParams& p, const VerifyPlan& plan, const CUtensorMap* tA,
                       const CUtensorMap* tS, double* part, cudaStream_t stream) {
-    switch (plan.ks) {
-        case 2: return launch_t<NWV, 2>(p, plan, tA, tS, part, stream);
-        case 4: return launch_t<NWV, 4>(p, plan, tA, tS, part, stream);
-        case 8: return launch_t<NWV, 8>(p, plan, tA, tS, part, stream);
-        case 12: return launch_t<NWV, 12>(p, plan, tA, tS, part, stream);
-        case 16: return launch_t<NWV, 16>(p, plan, tA, tS, part, stream);
-        default: return launch_t<NWV, 20>(p, plan, tA, tS, part, stream);
+    if constexpr (NWV == 4) {  // wide tiles only where C's fragments fit in registers
+        switch (plan.ks) {
+            case 2: return launch_t<NWV, 2>(p, plan, tA, tS, part, stream);
+            case 4: return launch_t<NWV, 4>(p, plan, tA, tS, part, stream);
+            case 8: return launch_t<NWV, 8>(p, plan, tA, tS, part, stream);
+            default: return cudaErrorInvalidValue;
+        }
+    } else {
+        switch (plan.ks) {
+            case 2: return launch_t<NWV, 2>(p, plan, tA, tS, part, stream);
+            case 4: return launch_t<NWV, 4>(p, plan, tA, tS, part, stream);
+            case 8: return launch_t<NWV, 8>(p, plan, tA, tS, part, stream);
+            case 12: return launch_t<NWV, 12>(p, plan, tA, tS, part, stream);
+            case 16: return launch_t<NWV, 16>(p, plan, tA, tS, part, stream);
+            default: return launch_t<NWV, 20>(p, plan, tA, tS, part, stream);
+        }
     }
 }
 
@@ -274,9 +283,10 @@ bool verify_make_plan(int64_t m, int64_t n, int64_t batch, int64_t kcap, int num
             ks = v;
             break;
         }
-    // column tile of 128 or 256 (16 warps x 8 x NWV); least padded work
+    // column tile of 128 or 256 (8 warps x 8 x NWV); least padded work; the
+    // wide tile keeps 16 DMMA accumulators per warp (ILP) when C fits in registers
     const int64_t c128 = ((n + 127) / 128) * 128, c256 = ((n + 255) / 256) * 256;
-    const int nwv = (c256 <= c128 && ks <= 8) ? 2 : 1;
+    const int nwv = (c256 <= c128 && ks <= 8) ? 4 : 2;
     plan->nwv = nwv;
     plan->ks = ks;
     plan->nt = kCons * 8 * nwv;
@@ -294,8 +304,8 @@ bool verify_make_plan(int64_t m, int64_t n, int64_t batch, int64_t kcap, int num
 
 cudaError_t launch_verify_tma(const VerifyParams& p, const VerifyPlan& plan, const CUtensorMap* tA,
                               const CUtensorMap* tS, double* part, cudaStream_t stream) {
-    return plan.nwv == 2 ? launch_ks<2>(p, plan, tA, tS, part, stream)
-                         : launch_ks<1>(p, plan, tA, tS, part, stream);
+    return plan.nwv == 4 ? launch_ks<4>(p, plan, tA, tS, part, stream)
+                         : launch_ks<2>(p, plan, tA, tS, part, stream);
 }
 
 }  // namespace spidgpu
