@@ -21,11 +21,13 @@
 //    transaction bytes, "empty" mbarriers collect one arrive per warp, so
 //    the main loop has no CTA-wide barrier at all. OOB rows/columns are
 //    zero-filled by the TMA unit (ragged m, n need no masking);
-//  * warps tile the CTA 2 (M) x 4 (N) (1 x 8 for ell <= 24); Omega never
-//    touches HBM or shared memory in performance mode: each lane runs the
-//    Philox generator for exactly the fragment values it feeds to DMMA (one
-//    call = 4 consecutive K of one row), one chunk ahead, interleaved with
-//    the tensor-core work of the current chunk;
+//  * warp specialisation: 4 producer warps (one per SMSP; one lane issues
+//    the TMA) write each chunk's Omega tile into a swizzled shared ring --
+//    read from the explicit Omega (oracle mode) or generated with Philox
+//    (the discretised Gaussian of philox.cuh; the Philox sketch normally runs
+//    on the integer kernels, this path serves SPIDGPU_OPT_DMMA_SKETCH) --
+//    while 16 consumer warps, tiled 2 (M) x 8 (N) (1 x 16 for ell <= 24),
+//    issue LDS.128 fragments and DMMA.8x8x4;
 //  * inside a 16-row chunk lane q feeds K = 4q + 2h + e at k-step (h, e), so
 //    each A fragment pair is one 16-byte shared load and the two rows of a
 //    quarter-warp hit opposite 16B-chunk parities under the swizzle: every

@@ -1,44 +1,45 @@
 // sketch_i8.cu -- the performance-mode sketch Y_s = Omega_s * A_s as an EXACT
-// integer-sliced contraction on the int8 tensor cores.
+// integer-sliced contraction on the register-fed int8 tensor path
+// (mma.sync m16n8k32, SASS IMMA.16832). The default kernel for this sketch is
+// sketch_tc.cu (tcgen05 + TMEM); this one is selected with
+// SPIDGPU_OPT_IMMA_SKETCH and kept for A/B measurement and tests.
 //
 // Same reference role as sketch.cu (the north star's Gaussian sketch in place
 // of subsample/subsample_column, proj/src/grid.cpp:136-150; CPU restatement
 // matmul(Omega, A), proj/src/dense_matrix.cpp:38-53), for the Philox Omega.
 //
-// Why: the DMMA sketch is bound by the FP64 tensor pipe (2*ell*m*n flop at
-// 37 TFLOP/s: 7.0 ms at config 3 against 3.3 ms to stream A from HBM). The
-// performance-mode Omega is integer-valued (Omega = Q/32, |Q| <= 117, see
-// philox.cuh), so Omega * A can be formed exactly from integer products:
-//
+// The performance-mode Omega is integer-valued (Omega = Q/32, |Q| <= 117, see
+// philox.cuh), so Omega * A is formed from exact integer products:
 //   * every column c of A gets a per-period exponent E_c (the largest
-//     exponent of its first 32 rows in the period + 8 bits of headroom), and
-//     each entry becomes the 63-bit fixed-point integer v = rint(x 2^(62-E_c))
-//     (one DMUL + F2I.S64); the error is 2^-63 of 2^E_c per entry, far below
-//     the fp64 rounding of a sequential sum;
-//   * v is split into 8 byte slices (bytes 0..6 unsigned, byte 7 signed) by a
-//     PRMT byte transpose that lands directly in the IMMA B-fragment layout;
-//   * each slice is contracted with Q on IMMA.16832 (mma.sync m16n8k32,
-//     s8 x u8 -> s32): exact, and |sum| < 2^31 for up to 65536 rows, so the
-//     int32 accumulators are flushed to fp64 every 2048 k-steps:
-//     Y += 2^(E_c - 67) * sum_t 2^(8t) D_t (two exact int64 partial sums);
+//     exponent of its first 64 rows in the period + 4 bits of headroom), and
+//     each entry becomes the fixed-point integer v = floor(x 2^(54-E_c)),
+//     formed on the FP64 pipe without F2I: t = RD(y + 1.5*2^84) holds
+//     floor(y / 2^32) in its low word, and RD((y - (t - 1.5*2^84)) + 2^52)
+//     holds the low 32 bits;
+//   * v is split into 7 byte slices (0..5 unsigned, 6 signed) by a PRMT byte
+//     transpose that lands directly in the IMMA B-fragment layout;
+//   * each slice is contracted with Q on IMMA.16832 (s8 x u8 -> s32): exact,
+//     and |sum| < 2^31 for up to 65536 rows, so the int32 accumulators are
+//     flushed to fp64 every 2048 k-steps: Y += 2^(E_c - 59) sum_t 2^(8t) D_t
+//     (two exact int64 partial sums);
 //   * a later entry with |x| >= 2^E_c (headroom exceeded) makes its warp flush
 //     and re-derive the exponents (warp-uniform slow path); a non-finite entry
 //     poisons its column to NaN, so the CPQR still raises NonFiniteInput.
 //
-// Per k-step of 32 rows a warp converts 256 entries of A and issues
-// 3 (ell 48) x 8 slices = 24 IMMAs: IMMA needs ~1.8 ms, F2I ~0.7 ms, PRMT
-// ~0.6 ms per config-3 step, all below the 3.3 ms of HBM streaming, so the
-// kernel is HBM-bound.
+// The IMMA issue rate (8 cycles per m16n8k32 per SMSP, profiles/
+// r01_int8_peak.txt) bounds this variant at ~4.3 ms per config-3 step (76%
+// of HBM); the tcgen05 kernel lifts that bound.
 //
 // Layout (B200): persistent grid, one CTA per SM, stream-K over
 // (subdomain, 64-column tile, 64-row chunk) exactly like sketch.cu; 8
-// consumer warps (n8 columns each, all ell rows) + 4 producer warps (TMA of
-// the A chunk as four 16x64 boxes with 128B swizzle, Philox + quantile table
-// lookups writing Omega straight into the IMMA A-fragment layout). Shared
-// loads of A are conflict-free: lane (g, q) reads 16B chunk q + 4((g&1)^i) of
-// column g, whose swizzled positions are distinct within each quarter-warp.
-// Partials go to the same [cta][seg][ell_pad][nt] workspace and fixed-order
-// reduction as sketch.cu, so Y is bitwise reproducible run to run.
+// consumer warps (n8 columns each, all ell rows, 224 registers via
+// setmaxnreg) + 4 producer warps (TMA of the A chunk as four 16x64 boxes
+// with 128B swizzle, Philox + quantile table lookups writing Omega straight
+// into the IMMA A-fragment layout). Shared loads of A are conflict-free:
+// lane (g, q) reads 16B chunk q + 4((g&1)^i) of column g, whose swizzled
+// positions are distinct within each quarter-warp. Partials go to the same
+// [cta][seg][ell_pad][nt] workspace and fixed-order reduction as sketch.cu,
+// so Y is bitwise reproducible run to run.
 #include <math.h>
 
 #include "common.cuh"
