@@ -109,7 +109,9 @@ int spidgpu_sketch_batched(spidgpu_handle h, const double* A, int64_t m, int64_t
                            double* Y, int64_t ldy, int64_t strideY, void* stream);
 
 /* Materialise the Omega_s that SPIDGPU_OMEGA_PHILOX uses (ell x m, ld ldo) so
- * an oracle can be fed the same bits. */
+ * an oracle can be fed the same bits: Omega_s(r, k) = Q[u >> 4] / 32 with u
+ * the 16-bit half (k % 8) of Philox4x32-7(counter {k / 8, r, s}, key seed) and
+ * Q the 4096-quantile table of N(0, 1) rounded to multiples of 1/32. */
 int spidgpu_philox_omega(spidgpu_handle h, uint64_t seed, int64_t subdomain, int64_t ell,
                          int64_t m, double* omega, int64_t ldo, void* stream);
 

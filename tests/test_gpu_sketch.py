@@ -64,7 +64,7 @@ def test_sketch_philox_matches_materialised_omega(engine, spid, orc):
     Y = engine.sketch(A, ell, seed=1234, subdomain_base=40)
     for s in range(3):
         om = spid.philox_omega(1234, 40 + s, ell, m)
-        # Gaussian moments of the generator (fp32 Box-Muller, widened)
+        # Gaussian moments of the generator (discretised N(0,1), Q/32)
         assert abs(om.mean()) < 0.02 and abs(om.std() - 1.0) < 0.02
         y_ref = orc.matmul(om, _host(A[s]))
         scale = np.linalg.norm(y_ref, axis=0)
