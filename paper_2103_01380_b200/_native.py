@@ -12,7 +12,8 @@ import re
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libspidgpu.so")
+# SPIDGPU_LIB_PATH: an alternative in-tree build (A/B experiments under tools/)
+LIB_PATH = os.environ.get("SPIDGPU_LIB_PATH") or os.path.join(HERE, "lib", "libspidgpu.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "spidgpu.h")
 
 RULE_FIXED, RULE_TOL, RULE_BLOCKED = 0, 1, 2

@@ -21,14 +21,15 @@
 // columns [N t, N t + N)) += slice_t(A^T) (128 x 32, K-major) *
 // Q^T (32 x N, K-major), one MMA per slice per 32-row stage.
 //
-// Warp roles (384 threads, persistent, one CTA per SM, stream-K over
+// Warp roles (512 threads, persistent, one CTA per SM, stream-K over
 // (subdomain, 128-column tile, 32-row stage) like sketch.cu):
-//   warps 0-3   Omega: Philox + quantile table -> K-major int8 tile, one
-//               warp per SMSP; warp 0's lane 0 also keeps the A ring full
-//               (two 16x128 fp64 TMA boxes, 128B swizzle, per stage), warp
-//               1 allocates TMEM and its lane 0 issues the 8 MMAs per stage
-//               (one stage behind), committed to the slot's "empty" mbarrier
-//   warps 4-11  converters, two per TMEM lane quarter, 16 columns each;
+//   warps 0-7   (80 registers) Omega: warps 0, 2..7 run Philox + quantile
+//               table -> K-major int8 tile, at most one task per lane per
+//               stage; warp 0's lane 0 also keeps the A ring full (two
+//               16x128 fp64 TMA boxes, 128B swizzle, per stage), warp 1
+//               allocates TMEM and its lane 0 issues the 8 MMAs per stage,
+//               committed to the slot's "empty" mbarrier
+//   warps 8-15  (176 registers) converters, two per TMEM lane quarter, 16 columns each;
 //               thread = (column, row half): 16 fp64 entries of the stage ->
 //               one DFMA each (offset-binary fixed point, below) -> 4x4 PRMT
 //               byte transposes -> one 16-byte store per slice into the
@@ -49,9 +50,14 @@ namespace spidgpu {
 
 namespace {
 
-constexpr int kThreads = 384;
-constexpr int kConvWarps = 8;         // warps 4..11: two per TMEM lane quarter
-constexpr int kGenWarps = 4;          // warps 0..3 (one per SMSP)
+constexpr int kThreads = 512;
+constexpr int kConvWarps = 8;         // warps 8..15: two per TMEM lane quarter
+constexpr int kGenWarps = 7;          // warps 0, 2..7 generate Omega (warp 1 issues the MMAs)
+// register split (setmaxnreg; launch budget 512 x 128): warpgroups 0-1 (TMA,
+// MMA, Omega) 80, warpgroups 2-3 (converters) 176
+constexpr int kAuxRegs = 80;
+constexpr int kConvRegs = 176;
+static_assert(8 * 32 * (kAuxRegs + kConvRegs) <= 65536, "register file");
 constexpr int kM = 128;               // snapshots per CTA tile (UMMA M)
 constexpr int kRows = 32;             // rows of A per stage (UMMA K for int8)
 constexpr int kSlices = 7;            // byte slices of the offset-binary fixed point
@@ -62,7 +68,6 @@ constexpr int kHeadroom = 3;
 // its low nibble 3 at bit 52), an unsigned 7-byte integer while |v| < 2^51
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
 constexpr int kOffsetHi = 7 << 19;             // kOffset = 7 * 2^51 = kOffsetHi * 2^32
-constexpr uint32_t kMagicHi = 0x43300000u;     // hi word of t while v is representable
 constexpr int kEbMin = 9;
 constexpr int kPeriodStages = 2048;   // 65536 rows: 65536 * 117 * 255 < 2^31
 constexpr int kBoxBytes = 16 * kM * 8;              // 16 rows x 128 columns fp64
@@ -144,12 +149,6 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                  : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-                 : "r"(taddr));
-}
-
 // .16x64b: the warp's 16 lanes from the address' lane field; thread t holds
 // lane 8 (t & 1) + (t >> 2), columns ((t >> 1) & 1) + 2 j (probed on B200:
 // tools/microbench/tmem_16dp.cu)
@@ -160,10 +159,6 @@ __device__ __forceinline__ void tmem_ld16x64b_x8(uint32_t taddr, uint32_t (&v)[8
 }
 __device__ __forceinline__ void tmem_st16x64b_x8_zero(uint32_t taddr) {
     asm volatile("tcgen05.st.sync.aligned.16x64b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(taddr), "r"(0u)
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_st8_zero(uint32_t taddr) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(taddr), "r"(0u)
                  : "memory");
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
@@ -229,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&a_empty[i], kConvWarps);
         }
         for (int i = 0; i < kBStages; ++i) {
-            mbar_init(&b_full[i], kConvWarps + kGenWarps - 1);
+            mbar_init(&b_full[i], kConvWarps + kGenWarps);
             mbar_init(&b_empty[i], 1);
         }
         fence_barrier_init();
@@ -244,12 +239,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp < 4) {
+    if (warp < 8) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kAuxRegs));
         // ------------------- Omega tiles (+ TMA on warp 0, MMA on warp 1) -------------------
-        // Warps 0, 2, 3 generate the Omega tile (warp 0's lane 0 also refills
+        // Warps 0, 2..7 generate the Omega tile (warp 0's lane 0 also refills
         // the A ring); warp 1's lane 0 only issues the MMAs, as soon as a
-        // stage's slices and Omega are complete.
-        constexpr int kTasksPerWarp = (2 * NPAD + 2) / 3;  // warps 0, 2, 3 share the Omega tile
+        // stage's slices and Omega are complete. A task is one Philox call
+        // (8 entries of one Omega row, an 8-byte store) when the tile has at
+        // most one per generator lane, else two (16 bytes): each lane runs at
+        // most one task per stage, so the tile's latency is one task's.
+        constexpr bool kFine = 4 * NPAD <= 32 * kGenWarps;
+        constexpr int kTasks = kFine ? 4 * NPAD : 2 * NPAD;
+        constexpr int kTasksPerWarp = (kTasks + kGenWarps - 1) / kGenWarps;
+        static_assert(kTasksPerWarp <= 32, "one Omega task per lane");
         const int gw = warp == 0 ? 0 : warp - 1;
 
         constexpr uint32_t kIdU = idesc_i8(NPAD, false);
@@ -287,25 +289,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else
         for (int it = 0; it < niter; ++it) {
             const int sl = it % kBStages;
-            if (it >= kBStages) mbar_wait(&b_empty[sl], ((it / kBStages) - 1) & 1);
             const uint32_t ot = b_s + sl * Cfg::kBStageBytes + kSlices * kSliceBytes;
             const uint32_t ko = static_cast<uint32_t>((cp.kc * kRows) >> 3);
-            for (int tk = lane; tk < kTasksPerWarp; tk += 32) {
-                const int task = gw * kTasksPerWarp + tk;
-                if (task >= 2 * NPAD) break;
-                const int r = task % NPAD, h = task / NPAD;  // row, 16-byte K half
-                uint32_t w[4] = {0u, 0u, 0u, 0u};
-                if (r < p.ell) {
+            const int task = gw * kTasksPerWarp + lane;
+            const bool has_task = lane < kTasksPerWarp && task < kTasks;
+            // row r, K octet(s) from o8: fine tasks one octet, else a 16-byte K half
+            const int r = task % NPAD, o8 = (kFine ? 1 : 2) * (task / NPAD);
+            constexpr int kOct = kFine ? 1 : 2;
+            uint32_t w[2 * kOct];
 #pragma unroll
-                    for (int o = 0; o < 2; ++o) {
-                        int q[8];
-                        omega_q8(p.seed, static_cast<uint64_t>(p.sub_base + cp.s), static_cast<uint32_t>(p.row0 + r),
-                                 ko + 2 * h + o, tab, q);
+            for (int i = 0; i < 2 * kOct; ++i) w[i] = 0u;
+            if (has_task && r < p.ell) {
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) w[2 * o + e / 4] |= static_cast<uint32_t>(q[e] & 0xff) << (8 * (e & 3));
-                    }
+                for (int o = 0; o < kOct; ++o) {
+                    int q[8];
+                    omega_q8(p.seed, static_cast<uint64_t>(p.sub_base + cp.s), static_cast<uint32_t>(p.row0 + r),
+                             ko + o8 + o, tab, q);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) w[2 * o + e / 4] |= static_cast<uint32_t>(q[e] & 0xff) << (8 * (e & 3));
                 }
-                sts128u(ot + h * (NPAD * 16) + r * 16, w[0], w[1], w[2], w[3]);
+            }
+            // generated ahead; only the store waits for the MMAs that read the slot
+            if (it >= kBStages) mbar_wait(&b_empty[sl], ((it / kBStages) - 1) & 1);
+            if (has_task) {
+                // K-major core-matrix layout: K half o8 / 2 at NPAD * 16 B, row r at 16 B
+                const uint32_t dst = ot + (o8 >> 1) * (NPAD * 16) + r * 16 + (o8 & 1) * 8;
+                if constexpr (kFine)
+                    sts64u(dst, w[0], w[1]);
+                else
+                    sts128u(dst, w[0], w[1], w[2 * kOct - 2], w[2 * kOct - 1]);
             }
             fence_proxy_async();
             __syncwarp();
@@ -321,16 +333,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
         }
     } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kConvRegs));
         // ------------------------------ converters ------------------------------
-        // Two warps per TMEM lane quarter: warp w (4..11) owns the 16 columns
-        // 32 (w % 4) + 16 hh + [0, 16) (hh = (w - 4) / 4) = those TMEM lanes,
+        // Two warps per TMEM lane quarter: warp w (8..15) owns the 16 columns
+        // 32 (w % 4) + 16 hh + [0, 16) (hh = (w - 8) / 4) = those TMEM lanes,
         // all 32 rows of every stage and all slices. Conversion: lane =
         // (column cc = lane & 15, row half b = lane >> 4), 16 entries each;
         // the two halves of a column share its exponent through one shuffle.
         // Flush: tcgen05.ld/st .16x64b touch only the warp's 16 lanes (lane L
         // = 8 (t & 1) + (t >> 2), column parity (t >> 1) & 1 per thread t), so
         // a column's overflow handling and flushes never involve another warp.
-        const int q = warp & 3, hh = (warp - 4) >> 2;
+        const int q = warp & 3, hh = (warp - 8) >> 2;
         const int cc = lane & 15, b = lane >> 4;
         const int col = q * 32 + hh * 16 + cc;
         const uint32_t lane_base = static_cast<uint32_t>(q * 32 + hh * 16) << 16;
@@ -447,8 +460,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const bool more = it + 1 < niter;
             if (more) load(it + 1, xn);
-            // the slice slot is free once the MMAs that read it completed
-            if (it >= kBStages) mbar_wait(&b_empty[sb], ((it / kBStages) - 1) & 1);
             // one DFMA per entry -- t = RN(x 2^(P-E) + 1.5 2^52), whose low 56
             // bits are u = rint(x 2^(P-E)) + kOffset -- then 4x4 PRMT byte
             // transposes and one 16-byte store per slice (K half b, row col).
@@ -485,6 +496,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         sw[6][g4] = __byte_perm(t1, t3, 0x5410);
                     }
                 }
+                // the slice slot is free once the MMAs that read it completed:
+                // only the stores wait, the conversion runs ahead
+                if (it >= kBStages) mbar_wait(&b_empty[sb], ((it / kBStages) - 1) & 1);
 #pragma unroll
                 for (int t = 0; t < kSlices; ++t) sts128u(st + t * kSliceBytes, sw[t][0], sw[t][1], sw[t][2], sw[t][3]);
             };
