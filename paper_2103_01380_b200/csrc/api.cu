@@ -106,7 +106,13 @@ int do_sketch(spidgpu_handle h, Workspace& ws, const double* A, int64_t m, int64
     const int kind = om->mode != SPIDGPU_OMEGA_PHILOX || h->force_dmma_sketch ? K_DMMA
                      : h->force_imma_sketch                                  ? K_IMMA
                                                                              : K_TC;
-    const int64_t slice = kind == K_TC ? kSketchTcMaxEll : kind == K_IMMA ? kSketchI8MaxEll : 80;
+    int64_t slice = kind == K_TC ? kSketchTcMaxEll : kind == K_IMMA ? kSketchI8MaxEll : 80;
+    if (kind == K_TC && ell > slice) {
+        // even passes of whole 16-row groups: ell = 80 runs as 48 + 32, not 64 + 16
+        // (the Omega/MMA work per A pass grows with the pass width)
+        const int64_t passes = (ell + slice - 1) / slice;
+        slice = std::min<int64_t>(16 * (((ell + passes - 1) / passes + 15) / 16), kSketchTcMaxEll);
+    }
     for (int64_t row0 = 0; row0 < ell; row0 += slice) {
         const int64_t ells = std::min<int64_t>(slice, ell - row0);
         SketchPlan plan;
