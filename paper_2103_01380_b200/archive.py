@@ -79,7 +79,13 @@ def compress_field(a, dims, blocks=None, strides=None, rank=None, tol=None, *, p
 
 
 def _buf(data):
-    b = np.frombuffer(bytes(data), dtype=np.uint8)
+    """Zero-copy uint8 view of an archive held in bytes / bytearray / mmap /
+    numpy memory (a page-locked buffer stays page-locked, so the library
+    uploads it directly instead of staging it)."""
+    if isinstance(data, np.ndarray):
+        b = np.ascontiguousarray(data).reshape(-1).view(np.uint8)
+    else:
+        b = np.frombuffer(memoryview(data).cast("B"), dtype=np.uint8)
     return b, C.c_void_p(b.ctypes.data if b.size else 0)
 
 

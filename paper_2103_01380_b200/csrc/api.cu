@@ -551,6 +551,9 @@ int spidgpu_destroy(spidgpu_handle h) {
     cudaDeviceSynchronize();
     for (auto& w : h->ws) w.release();
     if (h->archive_pinned) cudaFreeHost(h->archive_pinned);
+    if (h->upload_pinned) cudaFreeHost(h->upload_pinned);
+    for (cudaEvent_t e : h->upload_ev)
+        if (e) cudaEventDestroy(e);
     for (int i = 0; i < 2; ++i) {
         if (h->lanes[i]) cudaStreamDestroy(h->lanes[i]);
         if (h->ev[i]) cudaEventDestroy(h->ev[i]);

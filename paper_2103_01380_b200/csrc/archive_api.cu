@@ -9,6 +9,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <algorithm>
+#include <thread>
 #include <vector>
 
 #include "archive_internal.h"
@@ -284,6 +286,57 @@ int decode_checked(spidgpu_handle h, const uint8_t* bytes, const Framing& F,
     return SPID_OK;
 }
 
+// Host bytes -> device. Page-locked sources (spidgpu_archive_view, pinned
+// buffers) go straight to the copy engine; pageable ones (an archive read
+// from a file) would crawl through the driver's bounce buffer at ~10 GB/s,
+// so T host threads copy 4 MB chunks into their own two pinned slots while
+// the copy engine drains the previous ones.
+int upload_host_bytes(spidgpu_handle h, uint8_t* dst, const uint8_t* src, int64_t n, cudaStream_t st) {
+    constexpr int64_t kChunk = int64_t(4) << 20;
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, src) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    if (pinned || n < 2 * kChunk) {
+        CK(h, cudaMemcpyAsync(dst, src, static_cast<size_t>(n), cudaMemcpyHostToDevice, st));
+        return SPID_OK;
+    }
+    const int64_t nchunks = (n + kChunk - 1) / kChunk;
+    const unsigned hc = std::thread::hardware_concurrency();
+    const int T = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({8, hc ? hc / 2 : 4, (nchunks + 1) / 2})));
+    const size_t want = static_cast<size_t>(2 * T * kChunk);
+    for (cudaEvent_t e : h->upload_ev)  // slots of a previous call may still be draining
+        if (e) CK(h, cudaEventSynchronize(e));
+    if (h->upload_cap < want) {
+        if (h->upload_pinned) cudaFreeHost(h->upload_pinned);
+        h->upload_pinned = nullptr;
+        h->upload_cap = 0;
+        CK(h, cudaHostAlloc(reinterpret_cast<void**>(&h->upload_pinned), want, cudaHostAllocDefault));
+        h->upload_cap = want;
+    }
+    for (int i = 0; i < 2 * T; ++i)
+        if (!h->upload_ev[i]) CK(h, cudaEventCreateWithFlags(&h->upload_ev[i], cudaEventDisableTiming));
+    std::vector<cudaError_t> errs(T, cudaSuccess);
+    std::vector<std::thread> workers;
+    for (int w = 0; w < T; ++w)
+        workers.emplace_back([&, w] {
+            cudaError_t e = cudaSetDevice(h->device);
+            for (int64_t c = w, j = 0; c < nchunks && e == cudaSuccess; c += T, ++j) {
+                const int slot = 2 * w + static_cast<int>(j & 1);
+                uint8_t* buf = h->upload_pinned + slot * kChunk;
+                if (j >= 2) e = cudaEventSynchronize(h->upload_ev[slot]);
+                if (e != cudaSuccess) break;
+                const int64_t len = std::min(kChunk, n - c * kChunk);
+                std::memcpy(buf, src + c * kChunk, static_cast<size_t>(len));
+                e = cudaMemcpyAsync(dst + c * kChunk, buf, static_cast<size_t>(len), cudaMemcpyHostToDevice, st);
+                if (e == cudaSuccess) e = cudaEventRecord(h->upload_ev[slot], st);
+            }
+            errs[w] = e;
+        });
+    for (auto& t : workers) t.join();
+    for (cudaError_t e : errs) CK(h, e);
+    return SPID_OK;
+}
+
 int decode_archive(spidgpu_handle h, const uint8_t* bytes, int64_t nbytes, Decoded* out,
                    cudaStream_t st) {
     Framing F;
@@ -303,8 +356,8 @@ int decode_archive(spidgpu_handle h, const uint8_t* bytes, int64_t nbytes, Decod
     const size_t o_first = cv.take<int64_t>(first_part.size());
     const size_t o_pcrc = cv.take<uint32_t>(parts.size());
     CK(h, ws.bytes.ensure(cv.off, st));
-    CK(h, cudaMemcpyAsync(at<uint8_t>(ws.bytes, o_bytes), bytes, static_cast<size_t>(nbytes),
-                          cudaMemcpyHostToDevice, st));
+    int rc = upload_host_bytes(h, at<uint8_t>(ws.bytes, o_bytes), bytes, nbytes, st);
+    if (rc) return rc;
     CK(h, cudaMemcpyAsync(at<CrcSection>(ws.bytes, o_secs), secs.data(),
                           sizeof(CrcSection) * secs.size(), cudaMemcpyHostToDevice, st));
     CK(h, cudaMemcpyAsync(at<CrcPart>(ws.bytes, o_parts), parts.data(), sizeof(CrcPart) * parts.size(),
@@ -433,9 +486,10 @@ int spidgpu_crc32(spidgpu_handle h, const void* data, int64_t nbytes, int32_t on
     const size_t o_out = cv.take<uint32_t>(1);
     CK(h, ws.crc.ensure(cv.off, st));
     if (!on_device) {
-        if (nbytes)
-            CK(h, cudaMemcpyAsync(at<uint8_t>(ws.crc, o_data), data, static_cast<size_t>(nbytes),
-                                  cudaMemcpyHostToDevice, st));
+        if (nbytes) {
+            const int rc = upload_host_bytes(h, at<uint8_t>(ws.crc, o_data), src, nbytes, st);
+            if (rc) return rc;
+        }
         src = at<uint8_t>(ws.crc, o_data);
     }
     CK(h, launch_crc32(src, nbytes, at<uint32_t>(ws.crc, o_scr), at<uint32_t>(ws.crc, o_out), st));
@@ -816,7 +870,7 @@ int spidgpu_archive_decompress(spidgpu_handle h, const uint8_t* bytes, int64_t n
         p.mb = G.proto.l[0] * G.proto.l[1] * G.proto.l[2];
         p.kcap = 1;
         for (int64_t b : G.members) p.kcap = std::max(p.kcap, D.blocks[b].cr);
-        if (p.kcap > 200 * 1024 / (8 * 64)) return fail(h, SPID_SHAPE_UNSUPPORTED, "rank too large for decompress");
+        if (p.kcap > 200 * 1024 / (8 * 65)) return fail(h, SPID_SHAPE_UNSUPPORTED, "rank too large for decompress");
         if (G.coarse) {
             rc = local_spec(h, L, G.proto, strides3, D.meta.include_boundary ? 1 : 0, &p.g, &p.P, &p.Pc);
             if (rc) return rc;

@@ -85,6 +85,10 @@ struct spidgpu_context {
     bool force_imma_sketch = false;   // Philox sketches on register-fed IMMA instead of tcgen05
     uint8_t* archive_pinned = nullptr;  // last archive built by spidgpu_archive_compress
     size_t archive_cap = 0, archive_size = 0;
+    // pinned staging slots for pageable host uploads (upload_host_bytes)
+    uint8_t* upload_pinned = nullptr;
+    size_t upload_cap = 0;
+    cudaEvent_t upload_ev[16] = {};
 };
 
 namespace spidgpu {

@@ -59,6 +59,19 @@ def test_crc32_matches_zlib(A, n):
     assert A.crc32(data) == zlib.crc32(data)
 
 
+@pytest.mark.parametrize("n", [(8 << 20) + 3, (37 << 20) + 11])
+def test_crc32_staged_upload(A, n):
+    """Pageable host buffers >= 8 MB go through the threaded pinned staging
+    (4 MB chunks, ragged tail); a page-locked buffer of the same bytes is
+    copied directly. Both equal zlib."""
+    data = np.random.default_rng(n).integers(0, 256, n, dtype=np.uint8)
+    want = zlib.crc32(data.tobytes())
+    assert A.crc32(data.tobytes()) == want
+    pinned = torch.from_numpy(data).pin_memory()
+    assert A.crc32(pinned.numpy()) == want
+    assert A.crc32(data.tobytes()) == want  # staging slots reused across calls
+
+
 @pytest.mark.parametrize("off", [0, 1, 3, 8, 13])
 def test_crc32_device_unaligned(A, off):
     buf = torch.randint(0, 256, (70001,), dtype=torch.uint8, device="cuda")
@@ -220,3 +233,10 @@ def test_large_field_property_roundtrip(A):
     out = torch.empty((n, 128 ** 3), dtype=torch.float64, device="cuda").T
     A.decompress(data, out=out)
     assert torch.isfinite(out).all()
+    # the archive (> 8 MB) from pageable bytes went through the staged upload;
+    # from page-locked memory it is copied directly: same result bit for bit
+    assert len(data) > (8 << 20)
+    pinned = torch.frombuffer(bytearray(data), dtype=torch.uint8).pin_memory()
+    out2 = torch.empty_like(out.T).T
+    A.decompress(pinned.numpy(), out=out2)
+    assert torch.equal(out, out2)
