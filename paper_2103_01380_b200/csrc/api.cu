@@ -177,9 +177,12 @@ int do_cpqr(spidgpu_handle h, Workspace& ws, const double* Y, int64_t rows, int6
     const int64_t step_cap = std::max<int64_t>(1, ri.step_limit);
     const bool reg = cpqr_reg_supported(rows, n, step_cap) && !h->force_generic_cpqr;
     const bool w_smem = cpqr_smem_bytes(rows, n, step_cap, true) <= cpqr_max_dyn_smem();
+    // W too large for shared memory: tall inputs stream it through a TMA ring
+    const bool tall = !reg && !w_smem && cpqr_tall_supported(rows, n);
+    const int npad = tall ? cpqr_tall_npad(n) : static_cast<int>(n);
     CK(h, ws.rws.ensure(sizeof(double) * batch * step_cap * n, st));
     if (!reg && !w_smem) {
-        CK(h, ws.wws.ensure(sizeof(double) * batch * rows * n, st));
+        CK(h, ws.wws.ensure(sizeof(double) * batch * rows * npad, st));
         CK(h, ws.r11ws.ensure(sizeof(double) * batch * step_cap * step_cap, st));
     }
     CpqrParams p{};
@@ -197,7 +200,7 @@ int do_cpqr(spidgpu_handle h, Workspace& ws, const double* Y, int64_t rows, int6
     p.step_cap = step_cap;
     p.kcap = kcap;
     p.pre_status = ri.pre_status;
-    p.npad = static_cast<int>(n);
+    p.npad = npad;
     p.w_ws = ws.wws.as<double>();
     p.r_ws = ws.rws.as<double>();
     p.r11_ws = ws.r11ws.as<double>();
@@ -210,10 +213,24 @@ int do_cpqr(spidgpu_handle h, Workspace& ws, const double* Y, int64_t rows, int6
     p.pivots = pivots;
     p.Rout = R;
     p.Qout = Q;
-    if (reg)
+    if (reg) {
         CK(h, launch_cpqr_reg(p, st));
-    else
+    } else if (tall) {
+        CUtensorMap wmap;
+        cuuint64_t gdim[3] = {static_cast<cuuint64_t>(npad), static_cast<cuuint64_t>(rows),
+                              static_cast<cuuint64_t>(batch)};
+        cuuint64_t gstride[2] = {static_cast<cuuint64_t>(npad) * 8, static_cast<cuuint64_t>(rows) * npad * 8};
+        cuuint32_t box[3] = {static_cast<cuuint32_t>(npad), static_cast<cuuint32_t>(cpqr_tall_ring_rows(n)), 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        CUresult cr = h->encode(&wmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, ws.wws.ptr, gdim, gstride, box, estr,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (cr != CUDA_SUCCESS)
+            return fail(h, SPID_SHAPE_UNSUPPORTED, "cuTensorMapEncodeTiled (CPQR ring) failed: " + std::to_string(cr));
+        CK(h, launch_cpqr_tall(p, &wmap, st));
+    } else {
         CK(h, launch_cpqr(p, w_smem, st));
+    }
     h->launches += 1;
     return SPID_OK;
 }

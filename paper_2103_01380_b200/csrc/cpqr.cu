@@ -19,6 +19,16 @@
 // consecutive doubles per row -- conflict-free. Columns are never physically
 // swapped: perm[pos] / posof[col] carry the reference's position bookkeeping
 // (qr.cpp:83-87) and R is keyed by original column.
+//
+// Three placements of W (template kMode):
+//   0  W in shared memory (small inputs);
+//   1  W in global memory, each column-thread loading its rows directly;
+//   2  tall inputs (n <= 256): W in global memory streamed through a shared
+//      ring of row chunks by TMA (a dedicated producer warp, 5 x 32 KB
+//      stages): the column sweeps -- a sequential chain of DADDs per column --
+//      read their operands from shared memory instead of waiting on global
+//      loads. Mode 1 measured ~29 GB/s per SM on 4096 x 256 (memory-latency
+//      bound); the operation sequence is the same in all three modes.
 #include <math.h>
 
 #include "common.cuh"
@@ -34,6 +44,43 @@ constexpr double kCollapseRel = 1e-14; // qr.cpp:12
 
 constexpr int kPf = 32;  // rows per prefetched chunk of the column sweeps
 
+// mode 2: TMA ring of W row chunks
+#ifndef SPIDGPU_TALL_STAGE_KB
+#define SPIDGPU_TALL_STAGE_KB 32
+#define SPIDGPU_TALL_STAGES 5
+#endif
+constexpr int kTallStageBytes = SPIDGPU_TALL_STAGE_KB * 1024;
+constexpr int kTallStages = SPIDGPU_TALL_STAGES;
+constexpr int kProducerWarp = kCpqrThreads / kWarp;  // the extra (9th) warp
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+
+// CTA-wide barrier of the column threads (mode 2 excludes the producer warp)
+template <int kMode>
+__device__ __forceinline__ void csync() {
+    if constexpr (kMode == 2)
+        asm volatile("bar.sync 1, %0;\n" ::"n"(kCpqrThreads) : "memory");
+    else
+        __syncthreads();
+}
+template <int kMode>
+__device__ __forceinline__ int csync_or(int v) {
+    if constexpr (kMode == 2) {
+        int r;
+        asm volatile(
+            "{\n.reg .pred p, q;\nsetp.ne.s32 p, %1, 0;\nbar.red.or.pred q, 1, %2, p;\n"
+            "selp.s32 %0, 1, 0, q;\n}\n"
+            : "=r"(r)
+            : "r"(v), "n"(kCpqrThreads)
+            : "memory");
+        return r;
+    } else {
+        return __syncthreads_or(v);
+    }
+}
+
 // wv[u] = W[(i0 + u) * npad + col] for rows < `rows` (0 past the end).
 __device__ __forceinline__ void load_chunk(const double* W, int npad, int col, int i0, int rows,
                                            double (&wv)[kPf]) {
@@ -46,17 +93,20 @@ struct CpqrShared {
     int best_i;
     int stop;
     int flag;
+    int chunks;  // mode 2: row chunks the producer streams next (0 = exit)
     double max_init;
     double yfro;
 };
 
-template <bool kWInShared>
-__global__ void __launch_bounds__(kCpqrThreads)
-    cpqr_id_kernel(CpqrParams p) {
+template <int kMode>
+__global__ void __launch_bounds__(kMode == 2 ? kCpqrThreads + kWarp : kCpqrThreads)
+    cpqr_id_kernel(CpqrParams p, const __grid_constant__ CUtensorMap wmap, int ring_rows) {
+    constexpr bool kWInShared = kMode == 0;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ CpqrShared sh;
     __shared__ double red_v[kCpqrThreads / kWarp];
     __shared__ int red_i[kCpqrThreads / kWarp];
+    __shared__ uint64_t ring_full[kTallStages], ring_empty[kTallStages], go_bar;
 
     const int b = blockIdx.x;
     const int tid = threadIdx.x;
@@ -71,8 +121,16 @@ __global__ void __launch_bounds__(kCpqrThreads)
     int* posof;
     double* diag;  // R(t,t) in selection order (step_cap)
     double* r11;   // R11 in position order, rank x rank row-major (step_cap^2)
+    double* ring = nullptr;  // mode 2: kTallStages x ring_rows x npad
     {
         unsigned char* cur = smem_raw;
+        if constexpr (kMode == 2) {
+            // 128-byte aligned TMA destination, derived from smem_raw by an
+            // integer offset so the compiler keeps the shared address space (LDS)
+            cur += (128u - (smem_u32(smem_raw) & 127u)) & 127u;
+            ring = reinterpret_cast<double*>(cur);
+            cur += static_cast<size_t>(kTallStages) * kTallStageBytes;
+        }
         if (kWInShared) {
             W = reinterpret_cast<double*>(cur);
             cur += sizeof(double) * static_cast<size_t>(rows) * npad;
@@ -99,6 +157,76 @@ __global__ void __launch_bounds__(kCpqrThreads)
     double* R = p.r_ws + static_cast<size_t>(b) * p.step_cap * n;  // R[s][col]
     const double* Y = p.Y + static_cast<size_t>(b) * p.strideY;
 
+    // ---- mode 2: producer warp and the ring protocol -----------------------
+    // Passes are announced by thread 0 (sh.chunks, then an arrive on go_bar)
+    // after a barrier that follows a proxy fence of every thread's global
+    // writes, so a TMA read never overtakes the generic stores of the pass
+    // before. Every consumer warp releases every chunk (ring_empty count 8).
+    const int nck = kMode == 2 ? (rows + ring_rows - 1) / ring_rows : 0;
+    if constexpr (kMode == 2) {
+        if (tid == 0) {
+            for (int i = 0; i < kTallStages; ++i) {
+                mbar_init(&ring_full[i], 1);
+                mbar_init(&ring_empty[i], kCpqrThreads / kWarp);
+            }
+            mbar_init(&go_bar, 1);
+            fence_barrier_init();
+        }
+        __syncthreads();
+        if (warp == kProducerWarp) {
+            if (lane == 0) {
+                prefetch_tmap(&wmap);
+                const uint32_t bytes = static_cast<uint32_t>(ring_rows) * npad * sizeof(double);
+                uint32_t g = 0, gophase = 0;
+                for (;;) {
+                    mbar_wait(&go_bar, gophase);
+                    gophase ^= 1;
+                    const int chunks = sh.chunks;
+                    if (chunks == 0) break;
+                    for (int c = 0; c < chunks; ++c, ++g) {
+                        const uint32_t slot = g % kTallStages;
+                        if (g >= kTallStages) mbar_wait(&ring_empty[slot], ((g / kTallStages) - 1) & 1);
+                        mbar_arrive_expect_tx(&ring_full[slot], bytes);
+                        tma_load_3d(ring + static_cast<size_t>(slot) * (kTallStageBytes / sizeof(double)), &wmap,
+                                    &ring_full[slot], 0, (c % nck) * ring_rows, b);
+                    }
+                }
+            }
+            return;
+        }
+    }
+    uint32_t gcons = 0;  // consumer chunk counter (same sequence as the producer's)
+    // announce a pass of `passes` sweeps over W (after this thread's global writes)
+    auto start_sweeps = [&](int passes) {
+        if constexpr (kMode == 2) {
+            fence_proxy_async_global();
+            csync<kMode>();
+            if (tid == 0) {
+                sh.chunks = passes * nck;
+                mbar_arrive(&go_bar);
+            }
+        }
+    };
+    auto stop_producer = [&]() {
+        if constexpr (kMode == 2) {
+            if (tid == 0) {
+                sh.chunks = 0;
+                mbar_arrive(&go_bar);
+            }
+        }
+    };
+    // one sweep over W's rows: body(chunk in shared memory, first row, rows)
+    auto sweep = [&](auto&& body) {
+        for (int c = 0; c < nck; ++c, ++gcons) {
+            const uint32_t slot = gcons % kTallStages;
+            mbar_wait(&ring_full[slot], (gcons / kTallStages) & 1);
+            const int i0 = c * ring_rows;
+            body(ring + slot * (kTallStageBytes / sizeof(double)), i0, min(ring_rows, rows - i0));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ring_empty[slot]);
+        }
+    };
+
     // ---- load, transpose, finiteness (qr.cpp:34-35, id.cpp:41-42) -------
     int bad = 0;
     const int total = rows * n;
@@ -112,7 +240,7 @@ __global__ void __launch_bounds__(kCpqrThreads)
         perm[j] = j;
         posof[j] = j;
     }
-    bad = __syncthreads_or(bad);
+    bad = csync_or<kMode>(bad);
     auto finish_error = [&](int code) {
         if (tid == 0) {
             p.status[b] = code;
@@ -121,33 +249,55 @@ __global__ void __launch_bounds__(kCpqrThreads)
         }
     };
     if (bad) {
+        stop_producer();
         finish_error(SPID_NON_FINITE_INPUT);
         return;
     }
     if (p.pre_status != SPID_OK) {  // batch-uniform rule failures (qr.cpp:37-38)
+        stop_producer();
         finish_error(p.pre_status);
         return;
     }
 
     // ---- initial column norms, max_init (qr.cpp:47-51) -------------------
     double lmax = 0.0;
-    for (int j = tid; j < n; j += kCpqrThreads) {
+    if constexpr (kMode == 2) {  // n <= kCpqrThreads: at most one column per thread
+        start_sweeps(1);
+        const int j = tid;
         double s = 0.0;
-        for (int i0 = 0; i0 < rows; i0 += kPf) {
-            double wv[kPf];
-            load_chunk(W, npad, j, i0, rows, wv);
-#pragma unroll
-            for (int u = 0; u < kPf; ++u)
-                if (i0 + u < rows) s = add_rn(s, mul_rn(wv[u], wv[u]));
+        sweep([&](const double* ck, int, int nr) {
+            if (j < n)
+#pragma unroll 8
+                for (int u = 0; u < nr; ++u) {
+                    const double w = ck[u * npad + j];
+                    s = add_rn(s, mul_rn(w, w));
+                }
+        });
+        if (j < n) {
+            const double v = sqrt(s);
+            nrm[j] = v;
+            colsq[j] = s;
+            lmax = v;
         }
-        const double v = sqrt(s);
-        nrm[j] = v;
-        colsq[j] = s;
-        lmax = fmax(lmax, v);
+    } else {
+        for (int j = tid; j < n; j += kCpqrThreads) {
+            double s = 0.0;
+            for (int i0 = 0; i0 < rows; i0 += kPf) {
+                double wv[kPf];
+                load_chunk(W, npad, j, i0, rows, wv);
+#pragma unroll
+                for (int u = 0; u < kPf; ++u)
+                    if (i0 + u < rows) s = add_rn(s, mul_rn(wv[u], wv[u]));
+            }
+            const double v = sqrt(s);
+            nrm[j] = v;
+            colsq[j] = s;
+            lmax = fmax(lmax, v);
+        }
     }
     lmax = warp_max(lmax);
     if (lane == 0) red_v[warp] = lmax;
-    __syncthreads();
+    csync<kMode>();
     if (tid == 0) {
         double m = 0.0;
         for (int w = 0; w < kCpqrThreads / kWarp; ++w) m = fmax(m, red_v[w]);
@@ -160,9 +310,10 @@ __global__ void __launch_bounds__(kCpqrThreads)
             sh.yfro = sqrt(f);
         }
     }
-    __syncthreads();
+    csync<kMode>();
     const double max_init = sh.max_init;
     if (max_init < kZeroFloor) {
+        stop_producer();
         finish_error(SPID_ZERO_MATRIX);
         return;
     }
@@ -185,7 +336,7 @@ __global__ void __launch_bounds__(kCpqrThreads)
             red_v[warp] = bv;
             red_i[warp] = bi;
         }
-        __syncthreads();
+        csync<kMode>();
         if (tid == 0) {
             double v = red_v[0];
             int ix = red_i[0];
@@ -219,9 +370,10 @@ __global__ void __launch_bounds__(kCpqrThreads)
             sh.best_i = ix;
             sh.stop = stop;
         }
-        __syncthreads();
+        csync<kMode>();
         if (sh.stop) {
             if (sh.stop == 2) {
+                stop_producer();
                 finish_error(SPID_RANK_UNREACHABLE);
                 return;
             }
@@ -231,57 +383,101 @@ __global__ void __launch_bounds__(kCpqrThreads)
         const double pn = sh.best_v;
         // q_s = w_s / R(s,s) (qr.cpp:91-92)
         for (int i = tid; i < rows; i += kCpqrThreads) W[i * npad + pc] = div_rn(W[i * npad + pc], pn);
-        __syncthreads();
-        // two-pass MGS against every unselected column (qr.cpp:94-102); the
-        // next step's fresh norm (qr.cpp:66-67) is accumulated in pass 2.
-        for (int j = tid; j < n; j += kCpqrThreads) {
-            if (posof[j] <= s) continue;
-            // rows are consumed in chunks whose loads are all issued before the
-            // chunk's (sequential, separately rounded) arithmetic: the sums keep
-            // the reference's order, the memory latency is paid once per chunk
-            double r1 = 0.0;
-            for (int i0 = 0; i0 < rows; i0 += kPf) {
-                double qv[kPf], wv[kPf];
-                load_chunk(W, npad, pc, i0, rows, qv);
-                load_chunk(W, npad, j, i0, rows, wv);
-#pragma unroll
-                for (int u = 0; u < kPf; ++u)
-                    if (i0 + u < rows) r1 = add_rn(r1, mul_rn(qv[u], wv[u]));
-            }
-            double r2 = 0.0;
-            for (int i0 = 0; i0 < rows; i0 += kPf) {
-                double qv[kPf], wv[kPf];
-                load_chunk(W, npad, pc, i0, rows, qv);
-                load_chunk(W, npad, j, i0, rows, wv);
-#pragma unroll
-                for (int u = 0; u < kPf; ++u) {
-                    if (i0 + u < rows) {
-                        const double w = sub_rn(wv[u], mul_rn(r1, qv[u]));
-                        W[(i0 + u) * npad + j] = w;
-                        r2 = add_rn(r2, mul_rn(qv[u], w));
+        if constexpr (kMode == 2) {
+            // two-pass MGS (qr.cpp:94-102) over the TMA ring, as three read
+            // sweeps of the step's W that stream back to back (nothing is
+            // stored before the last): r1; then w' = w - r1 q and r2; then w'
+            // recomputed from w by the same two rounded operations, w'' =
+            // w' - r2 q stored and its norm. One W store per step instead of two.
+            const int j = tid;
+            const bool act = j < n && posof[j] > s;
+            start_sweeps(3);
+            double r1 = 0.0, r2 = 0.0, nn = 0.0;
+            double* Wj = W + j;
+            sweep([&](const double* ck, int, int nr) {
+                if (act)
+#pragma unroll 8
+                    for (int u = 0; u < nr; ++u) r1 = add_rn(r1, mul_rn(ck[u * npad + pc], ck[u * npad + j]));
+            });
+            sweep([&](const double* ck, int, int nr) {
+                if (act)
+#pragma unroll 8
+                    for (int u = 0; u < nr; ++u) {
+                        const double q = ck[u * npad + pc];
+                        r2 = add_rn(r2, mul_rn(q, sub_rn(ck[u * npad + j], mul_rn(r1, q))));
                     }
-                }
-            }
-            double nn = 0.0;
-            for (int i0 = 0; i0 < rows; i0 += kPf) {
-                double qv[kPf], wv[kPf];
-                load_chunk(W, npad, pc, i0, rows, qv);
-                load_chunk(W, npad, j, i0, rows, wv);
-#pragma unroll
-                for (int u = 0; u < kPf; ++u) {
-                    if (i0 + u < rows) {
-                        const double w = sub_rn(wv[u], mul_rn(r2, qv[u]));
-                        W[(i0 + u) * npad + j] = w;
+            });
+            sweep([&](const double* ck, int i0, int nr) {
+                if (act)
+#pragma unroll 8
+                    for (int u = 0; u < nr; ++u) {
+                        const double q = ck[u * npad + pc];
+                        const double w = sub_rn(sub_rn(ck[u * npad + j], mul_rn(r1, q)), mul_rn(r2, q));
+                        Wj[(i0 + u) * npad] = w;
                         nn = add_rn(nn, mul_rn(w, w));
                     }
-                }
+            });
+            if (act) {
+                R[static_cast<size_t>(s) * n + j] = add_rn(r1, r2);
+                nrm[j] = sqrt(nn);
             }
-            R[static_cast<size_t>(s) * n + j] = add_rn(r1, r2);
-            nrm[j] = sqrt(nn);
+            // the next step's argmax and normalisation follow a barrier
+            fence_proxy_async_global();
+            csync<kMode>();
+        } else {
+            __syncthreads();
+            // two-pass MGS against every unselected column (qr.cpp:94-102); the
+            // next step's fresh norm (qr.cpp:66-67) is accumulated in pass 2.
+            for (int j = tid; j < n; j += kCpqrThreads) {
+                if (posof[j] <= s) continue;
+                // rows are consumed in chunks whose loads are all issued before the
+                // chunk's (sequential, separately rounded) arithmetic: the sums keep
+                // the reference's order, the memory latency is paid once per chunk
+                double r1 = 0.0;
+                for (int i0 = 0; i0 < rows; i0 += kPf) {
+                    double qv[kPf], wv[kPf];
+                    load_chunk(W, npad, pc, i0, rows, qv);
+                    load_chunk(W, npad, j, i0, rows, wv);
+#pragma unroll
+                    for (int u = 0; u < kPf; ++u)
+                        if (i0 + u < rows) r1 = add_rn(r1, mul_rn(qv[u], wv[u]));
+                }
+                double r2 = 0.0;
+                for (int i0 = 0; i0 < rows; i0 += kPf) {
+                    double qv[kPf], wv[kPf];
+                    load_chunk(W, npad, pc, i0, rows, qv);
+                    load_chunk(W, npad, j, i0, rows, wv);
+#pragma unroll
+                    for (int u = 0; u < kPf; ++u) {
+                        if (i0 + u < rows) {
+                            const double w = sub_rn(wv[u], mul_rn(r1, qv[u]));
+                            W[(i0 + u) * npad + j] = w;
+                            r2 = add_rn(r2, mul_rn(qv[u], w));
+                        }
+                    }
+                }
+                double nn = 0.0;
+                for (int i0 = 0; i0 < rows; i0 += kPf) {
+                    double qv[kPf], wv[kPf];
+                    load_chunk(W, npad, pc, i0, rows, qv);
+                    load_chunk(W, npad, j, i0, rows, wv);
+#pragma unroll
+                    for (int u = 0; u < kPf; ++u) {
+                        if (i0 + u < rows) {
+                            const double w = sub_rn(wv[u], mul_rn(r2, qv[u]));
+                            W[(i0 + u) * npad + j] = w;
+                            nn = add_rn(nn, mul_rn(w, w));
+                        }
+                    }
+                }
+                R[static_cast<size_t>(s) * n + j] = add_rn(r1, r2);
+                nrm[j] = sqrt(nn);
+            }
+            __syncthreads();
         }
-        __syncthreads();
         rank = s + 1;
     }
+    stop_producer();
     if (rank == 0) {  // qr.cpp:108-109
         finish_error(SPID_ZERO_MATRIX);
         return;
@@ -311,7 +507,7 @@ __global__ void __launch_bounds__(kCpqrThreads)
             Qo[static_cast<size_t>(t) * rows + i] = W[i * npad + perm[t]];
         }
     }
-    __syncthreads();
+    csync<kMode>();
     if (sh.flag && rank < n) {
         finish_error(SPID_SINGULAR_PIVOT);
         return;
@@ -329,7 +525,7 @@ __global__ void __launch_bounds__(kCpqrThreads)
     for (int j = tid; j < n; j += kCpqrThreads)
         if (posof[j] >= rank)
             for (int t = 0; t < rank; ++t) X[t * npad + j] = R[static_cast<size_t>(t) * n + j];
-    __syncthreads();
+    csync<kMode>();
     double* C = p.C + static_cast<size_t>(b) * p.strideC;
     const int kcap = static_cast<int>(p.kcap);
     int nonfinite = 0;
@@ -351,7 +547,7 @@ __global__ void __launch_bounds__(kCpqrThreads)
         }
         for (int i = 0; i < rank; ++i) cj[i] = X[i * npad + j];
     }
-    nonfinite = __syncthreads_or(nonfinite);
+    nonfinite = csync_or<kMode>(nonfinite);
     if (nonfinite) {  // id.cpp:25-26
         finish_error(SPID_NON_FINITE_COEFFS);
         return;
@@ -386,25 +582,46 @@ size_t cpqr_smem_bytes(int64_t rows, int64_t n, int64_t step_cap, bool w_in_shar
 
 size_t cpqr_max_dyn_smem() { return 200 * 1024; }
 
+bool cpqr_tall_supported(int64_t rows, int64_t n) { return n <= kCpqrThreads && rows >= 256; }
+
+int cpqr_tall_npad(int64_t n) { return static_cast<int>((n + 1) & ~int64_t(1)); }  // 16-byte TMA rows
+
+int cpqr_tall_ring_rows(int64_t n) {  // a multiple of 8 (the sweeps' row groups), <= 256 (TMA box)
+    const int npad = cpqr_tall_npad(n);
+    const int r = (kTallStageBytes / (npad * static_cast<int>(sizeof(double)))) & ~7;
+    return r > 256 ? 256 : r;
+}
+
 cudaError_t launch_cpqr(const CpqrParams& p, bool w_in_shared, cudaStream_t stream) {
     const size_t smem = cpqr_smem_bytes(p.rows, p.n, p.step_cap, w_in_shared);
+    CUtensorMap none{};
     if (w_in_shared) {
         if (smem > 48 * 1024) {
-            cudaError_t e = cudaFuncSetAttribute(cpqr_id_kernel<true>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaError_t e = cudaFuncSetAttribute(cpqr_id_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  static_cast<int>(smem));
             if (e != cudaSuccess) return e;
         }
-        cpqr_id_kernel<true><<<static_cast<unsigned>(p.batch), kCpqrThreads, smem, stream>>>(p);
+        cpqr_id_kernel<0><<<static_cast<unsigned>(p.batch), kCpqrThreads, smem, stream>>>(p, none, 0);
     } else {
         if (smem > 48 * 1024) {
-            cudaError_t e = cudaFuncSetAttribute(cpqr_id_kernel<false>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaError_t e = cudaFuncSetAttribute(cpqr_id_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  static_cast<int>(smem));
             if (e != cudaSuccess) return e;
         }
-        cpqr_id_kernel<false><<<static_cast<unsigned>(p.batch), kCpqrThreads, smem, stream>>>(p);
+        cpqr_id_kernel<1><<<static_cast<unsigned>(p.batch), kCpqrThreads, smem, stream>>>(p, none, 0);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cpqr_tall(const CpqrParams& p, const CUtensorMap* wmap, cudaStream_t stream) {
+    if (!cpqr_tall_supported(p.rows, p.n) || p.npad != cpqr_tall_npad(p.n)) return cudaErrorInvalidValue;
+    const size_t smem = 128 + static_cast<size_t>(kTallStages) * kTallStageBytes +
+                        cpqr_smem_bytes(p.rows, p.n, p.step_cap, false);
+    cudaError_t e = cudaFuncSetAttribute(cpqr_id_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    cpqr_id_kernel<2><<<static_cast<unsigned>(p.batch), kCpqrThreads + kWarp, smem, stream>>>(
+        p, *wmap, cpqr_tall_ring_rows(p.n));
     return cudaGetLastError();
 }
 

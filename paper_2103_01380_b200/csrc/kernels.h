@@ -40,6 +40,12 @@ struct CpqrParams {
 size_t cpqr_smem_bytes(int64_t rows, int64_t n, int64_t step_cap, bool w_in_shared);
 size_t cpqr_max_dyn_smem();
 cudaError_t launch_cpqr(const CpqrParams& p, bool w_in_shared, cudaStream_t stream);
+// tall inputs (rows >= 256, n <= 256): W in global memory, streamed through a
+// TMA ring; wmap = 3D map {npad, rows, batch} of w_ws, box {npad, ring_rows, 1}
+bool cpqr_tall_supported(int64_t rows, int64_t n);
+int cpqr_tall_npad(int64_t n);
+int cpqr_tall_ring_rows(int64_t n);
+cudaError_t launch_cpqr_tall(const CpqrParams& p, const CUtensorMap* wmap, cudaStream_t stream);
 // register-resident variant for sketch-sized inputs (rows <= 80, n <= 512)
 bool cpqr_reg_supported(int64_t rows, int64_t n, int64_t step_cap);
 cudaError_t launch_cpqr_reg(const CpqrParams& p, cudaStream_t stream);

@@ -17,3 +17,4 @@ eng = Engine(0)
 A = eng.generate(field, first, count)
 torch.cuda.synchronize()
 print(bench.archive_measure(cfg, A, types.SimpleNamespace()), flush=True)
+print(bench.pipeline_measure(cfg, A, types.SimpleNamespace()), flush=True)
