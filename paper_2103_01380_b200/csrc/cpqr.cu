@@ -394,28 +394,51 @@ __global__ void __launch_bounds__(kMode == 2 ? kCpqrThreads + kWarp : kCpqrThrea
             start_sweeps(3);
             double r1 = 0.0, r2 = 0.0, nn = 0.0;
             double* Wj = W + j;
+            // rows of a chunk in order: whole groups of 8 with the next group's
+            // (q, w) loaded before the current group's dependent chain (the
+            // last group reloads itself, branch-free), then the ragged tail
+            auto rows = [&](const double* ck, int nr, auto&& f) {
+                const int nfull = nr & ~7;
+                if (nfull) {
+                    double qa[8], wa[8];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) {
+                        qa[t] = ck[t * npad + pc];
+                        wa[t] = ck[t * npad + j];
+                    }
+                    for (int u0 = 0; u0 < nfull; u0 += 8) {
+                        const int un = min(u0 + 8, nfull - 8);
+                        double qb[8], wb[8];
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            qb[t] = ck[(un + t) * npad + pc];
+                            wb[t] = ck[(un + t) * npad + j];
+                        }
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) f(u0 + t, qa[t], wa[t]);
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            qa[t] = qb[t];
+                            wa[t] = wb[t];
+                        }
+                    }
+                }
+                for (int u = nfull; u < nr; ++u) f(u, ck[u * npad + pc], ck[u * npad + j]);
+            };
             sweep([&](const double* ck, int, int nr) {
-                if (act)
-#pragma unroll 8
-                    for (int u = 0; u < nr; ++u) r1 = add_rn(r1, mul_rn(ck[u * npad + pc], ck[u * npad + j]));
+                if (act) rows(ck, nr, [&](int, double q, double w) { r1 = add_rn(r1, mul_rn(q, w)); });
             });
             sweep([&](const double* ck, int, int nr) {
                 if (act)
-#pragma unroll 8
-                    for (int u = 0; u < nr; ++u) {
-                        const double q = ck[u * npad + pc];
-                        r2 = add_rn(r2, mul_rn(q, sub_rn(ck[u * npad + j], mul_rn(r1, q))));
-                    }
+                    rows(ck, nr, [&](int, double q, double w) { r2 = add_rn(r2, mul_rn(q, sub_rn(w, mul_rn(r1, q)))); });
             });
             sweep([&](const double* ck, int i0, int nr) {
                 if (act)
-#pragma unroll 8
-                    for (int u = 0; u < nr; ++u) {
-                        const double q = ck[u * npad + pc];
-                        const double w = sub_rn(sub_rn(ck[u * npad + j], mul_rn(r1, q)), mul_rn(r2, q));
+                    rows(ck, nr, [&](int u, double q, double w0) {
+                        const double w = sub_rn(sub_rn(w0, mul_rn(r1, q)), mul_rn(r2, q));
                         Wj[(i0 + u) * npad] = w;
                         nn = add_rn(nn, mul_rn(w, w));
-                    }
+                    });
             });
             if (act) {
                 R[static_cast<size_t>(s) * n + j] = add_rn(r1, r2);
