@@ -87,10 +87,14 @@ int64_t spidgpu_launch_count(spidgpu_handle h);
  * SPIDGPU_OPT_DMMA_SKETCH = 2 runs Philox-Omega sketches on the FP64 DMMA
  * kernel, SPIDGPU_OPT_IMMA_SKETCH = 3 on the register-fed IMMA variant of
  * the exact integer-sliced contraction, instead of its tcgen05 (TMEM) kernel
- * (same Omega; the options exist for tests and A/B measurement). */
+ * (same Omega; the options exist for tests and A/B measurement).
+ * SPIDGPU_OPT_SKETCH_SMS = 4 caps the SMs the persistent sketch kernels
+ * occupy (0 = all), leaving the rest to kernels on other streams (the
+ * overlapped compress pipeline). */
 #define SPIDGPU_OPT_GENERIC_CPQR 1
 #define SPIDGPU_OPT_DMMA_SKETCH 2
 #define SPIDGPU_OPT_IMMA_SKETCH 3
+#define SPIDGPU_OPT_SKETCH_SMS 4
 int spidgpu_set_option(spidgpu_handle h, int option, int64_t value);
 
 /* =====================================================================

@@ -22,6 +22,7 @@ FIELD_TGV4, FIELD_TGV5, FIELD_MULTIMODE = 0, 1, 2
 SPIDGPU_OPT_GENERIC_CPQR = 1
 SPIDGPU_OPT_DMMA_SKETCH = 2
 SPIDGPU_OPT_IMMA_SKETCH = 3
+SPIDGPU_OPT_SKETCH_SMS = 4
 
 
 class SpidError(RuntimeError):

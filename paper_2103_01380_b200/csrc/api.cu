@@ -116,9 +116,10 @@ int do_sketch(spidgpu_handle h, Workspace& ws, const double* A, int64_t m, int64
     for (int64_t row0 = 0; row0 < ell; row0 += slice) {
         const int64_t ells = std::min<int64_t>(slice, ell - row0);
         SketchPlan plan;
-        const bool planned = kind == K_TC ? sketch_tc_make_plan(m, n, batch, ells, h->num_sms, &plan)
-                             : kind == K_IMMA ? sketch_i8_make_plan(m, n, batch, ells, h->num_sms, &plan)
-                                              : sketch_make_plan(m, n, batch, ells, h->num_sms, &plan);
+        const int sms = h->sketch_sms > 0 ? h->sketch_sms : h->num_sms;
+        const bool planned = kind == K_TC ? sketch_tc_make_plan(m, n, batch, ells, sms, &plan)
+                             : kind == K_IMMA ? sketch_i8_make_plan(m, n, batch, ells, sms, &plan)
+                                              : sketch_make_plan(m, n, batch, ells, sms, &plan);
         if (!planned) return fail(h, SPID_SHAPE_UNSUPPORTED, "no sketch plan");
         CK(h, ws.partial.ensure(plan.partial_elems * sizeof(double), st));
         CUtensorMap tmap;
@@ -589,6 +590,10 @@ int spidgpu_set_option(spidgpu_handle h, int option, int64_t value) {
         case SPIDGPU_OPT_GENERIC_CPQR: h->force_generic_cpqr = value != 0; return SPID_OK;
         case SPIDGPU_OPT_DMMA_SKETCH: h->force_dmma_sketch = value != 0; return SPID_OK;
         case SPIDGPU_OPT_IMMA_SKETCH: h->force_imma_sketch = value != 0; return SPID_OK;
+        case SPIDGPU_OPT_SKETCH_SMS:
+            if (value < 0) return SPID_INVALID_ARGUMENT;
+            h->sketch_sms = static_cast<int>(std::min<int64_t>(value, h->num_sms));
+            return SPID_OK;
         default: return SPID_INVALID_ARGUMENT;
     }
 }
