@@ -98,7 +98,9 @@ struct CpqrShared {
     double yfro;
 };
 
-template <int kMode>
+// kNpad: W's row length as a compile-time constant (0 = runtime p.npad), so
+// the tall sweeps' shared-memory addresses fold into immediate offsets
+template <int kMode, int kNpad = 0>
 __global__ void __launch_bounds__(kMode == 2 ? kCpqrThreads + kWarp : kCpqrThreads)
     cpqr_id_kernel(CpqrParams p, const __grid_constant__ CUtensorMap wmap, int ring_rows) {
     constexpr bool kWInShared = kMode == 0;
@@ -112,7 +114,7 @@ __global__ void __launch_bounds__(kMode == 2 ? kCpqrThreads + kWarp : kCpqrThrea
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     const int rows = static_cast<int>(p.rows), n = static_cast<int>(p.n);
-    const int npad = p.npad;
+    const int npad = kNpad ? kNpad : p.npad;
 
     double* W;
     double* nrm;
@@ -636,16 +638,27 @@ cudaError_t launch_cpqr(const CpqrParams& p, bool w_in_shared, cudaStream_t stre
     return cudaGetLastError();
 }
 
+template <int kNpad>
+cudaError_t launch_tall_t(const CpqrParams& p, const CUtensorMap* wmap, size_t smem, cudaStream_t stream) {
+    auto kern = cpqr_id_kernel<2, kNpad>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<static_cast<unsigned>(p.batch), kCpqrThreads + kWarp, smem, stream>>>(p, *wmap, cpqr_tall_ring_rows(p.n));
+    return cudaGetLastError();
+}
+
 cudaError_t launch_cpqr_tall(const CpqrParams& p, const CUtensorMap* wmap, cudaStream_t stream) {
     if (!cpqr_tall_supported(p.rows, p.n) || p.npad != cpqr_tall_npad(p.n)) return cudaErrorInvalidValue;
     const size_t smem = 128 + static_cast<size_t>(kTallStages) * kTallStageBytes +
                         cpqr_smem_bytes(p.rows, p.n, p.step_cap, false);
-    cudaError_t e = cudaFuncSetAttribute(cpqr_id_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    cpqr_id_kernel<2><<<static_cast<unsigned>(p.batch), kCpqrThreads + kWarp, smem, stream>>>(
-        p, *wmap, cpqr_tall_ring_rows(p.n));
-    return cudaGetLastError();
+    switch (p.npad) {  // the streaming pipeline's chunk widths and the archive's snapshot counts
+        case 16: return launch_tall_t<16>(p, wmap, smem, stream);
+        case 32: return launch_tall_t<32>(p, wmap, smem, stream);
+        case 64: return launch_tall_t<64>(p, wmap, smem, stream);
+        case 128: return launch_tall_t<128>(p, wmap, smem, stream);
+        case 256: return launch_tall_t<256>(p, wmap, smem, stream);
+        default: return launch_tall_t<0>(p, wmap, smem, stream);
+    }
 }
 
 }  // namespace spidgpu

@@ -1,5 +1,6 @@
 """Tall column IDs (rows >= 256, W too large for shared memory, n <= 256): the
-CPQR kernel streams W through a TMA ring of row chunks (cpqr.cu, mode 2).
+CPQR kernel streams W through a TMA ring of row chunks (cpqr.cu, mode 2;
+compile-time row lengths 16/32/64/128/256 and the runtime one are all hit).
 Same bar as every CPQR path: bit-exact pivots, R, Q, coefficients and
 residual against the oracle, including the error exits (the producer warp
 must be released on every one of them, or the launch would hang)."""
@@ -15,7 +16,8 @@ def _eq(a, b):
 
 
 @pytest.mark.parametrize("m,n,k", [(4096, 32, 16), (1000, 256, 32), (3001, 7, 5), (2500, 130, 40),
-                                   (257, 255, 60), (70000, 3, 3)])
+                                   (257, 255, 60), (70000, 3, 3), (5000, 16, 16), (2000, 128, 20),
+                                   (1777, 63, 30)])
 def test_tall_fixed_rank_bitwise(spid, orc, m, n, k):
     a = orc.seeded_matrix(m, n, 5 + m + n)
     g = spid.column_id(a, rank=k)
