@@ -1,5 +1,5 @@
-"""Where the streaming pipeline's host-frame e2e time goes: the push loop
-(one pinned host frame per call), spidgpu_stream_finish, and the copy of the
+"""Where the streaming pipeline's time goes: the push loop (device frames, or
+one pinned host frame per call), spidgpu_stream_finish, and the copy of the
 archive into Python bytes. python tools/exp_pipeline_e2e.py"""
 import ctypes as C
 import sys
@@ -18,16 +18,18 @@ eng = Engine(0)
 A = eng.generate(field_cfg, first, count)
 field = bench.global_field(A, cfg.grid, cfg.block, qoi=1)
 m, n = field.shape
+frames = field.T
 host = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
-host.copy_(field.T)
+host.copy_(frames)
 hf = host.numpy()
 pc = PL.StreamConfig(dims=(cfg.grid,) * 3, blocks=(cfg.grid // cfg.block,) * 3, strides=(2, 2, 2), time_chunk=32,
                      stage1_rank=16, stage2_tol=1e-5, periodic=(1, 1, 1), qoi="u", provenance="bench")
-for rep in range(3):
+for src_name, src in (("device", frames), ("host", hf)) * 3:
+    torch.cuda.synchronize()
     with PL.Pipeline(pc) as p:
         t0 = time.perf_counter()
         for j in range(n):
-            p.push(hf[j])
+            p.push(src[j])
         t1 = time.perf_counter()
         nb = C.c_int64()
         p._check(N.lib.spidgpu_stream_finish(p.s, C.byref(nb)))
@@ -37,6 +39,6 @@ for rep in range(3):
         data = C.string_at(view.value, ln.value)
         t3 = time.perf_counter()
         st = p.stats()
-    print(f"rep {rep}: push loop {1e3 * (t1 - t0):.1f} ms ({1e3 * (t1 - t0) / n:.3f} ms/frame), finish "
-          f"{1e3 * (t2 - t1):.1f} ms, bytes copy {1e3 * (t3 - t2):.1f} ms, total {1e3 * (t3 - t0):.1f} ms; "
-          f"stage1 {st['stage1_ms']:.1f} stage2 {st['stage2_ms']:.1f}", flush=True)
+    print(f"{src_name}: push loop {1e3 * (t1 - t0):.1f} ms, finish {1e3 * (t2 - t1):.1f} ms, bytes copy "
+          f"{1e3 * (t3 - t2):.1f} ms, total {1e3 * (t2 - t0):.1f} ms; stage1 {st['stage1_ms']:.1f} "
+          f"stage2 {st['stage2_ms']:.1f}", flush=True)
