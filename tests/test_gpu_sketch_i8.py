@@ -136,6 +136,22 @@ def test_i8_deterministic_and_partition_independent(engine):
     assert ((y3[0] - y1[3]).abs() / scale).max().item() <= 1e-14
 
 
+@pytest.mark.parametrize("sms", [1, 37, 132])
+def test_i8_sketch_sm_cap(engine, spid, orc, sms):
+    """SPIDGPU_OPT_SKETCH_SMS: a persistent grid capped to fewer SMs (other
+    stream-K splits) still matches the oracle, and resets to all SMs."""
+    from paper_2103_01380_b200 import _native as N
+
+    torch.manual_seed(5)
+    A = torch.randn((3, 200, 9000), dtype=torch.float64, device="cuda")
+    try:
+        engine.h.check(N.lib.spidgpu_set_option(engine.h.h, N.SPIDGPU_OPT_SKETCH_SMS, sms))
+        _check_vs_oracle(engine, spid, orc, A, 40, 21, 0)
+    finally:
+        engine.h.check(N.lib.spidgpu_set_option(engine.h.h, N.SPIDGPU_OPT_SKETCH_SMS, 0))
+    assert N.lib.spidgpu_set_option(engine.h.h, N.SPIDGPU_OPT_SKETCH_SMS, -1) != 0
+
+
 def test_i8_large_subdomain_cfg3_shape(engine, spid, orc):
     """One config-3 subdomain (163840 x 256, three flush periods)."""
     from paper_2103_01380_b200.configs import CONFIGS
