@@ -90,11 +90,16 @@ int64_t spidgpu_launch_count(spidgpu_handle h);
  * (same Omega; the options exist for tests and A/B measurement).
  * SPIDGPU_OPT_SKETCH_SMS = 4 caps the SMs the persistent sketch kernels
  * occupy (0 = all), leaving the rest to kernels on other streams (the
- * overlapped compress pipeline). */
+ * overlapped compress pipeline).
+ * SPIDGPU_OPT_SKETCH_PAIRS = 5 runs the tcgen05 sketch as clusters of two
+ * CTAs that share each stage's Omega tile: 0 never, 1 (default) where it
+ * measured faster (64-row passes), 2 whenever the column tiles pair up (same
+ * results to the parity bound; tests and A/B). */
 #define SPIDGPU_OPT_GENERIC_CPQR 1
 #define SPIDGPU_OPT_DMMA_SKETCH 2
 #define SPIDGPU_OPT_IMMA_SKETCH 3
 #define SPIDGPU_OPT_SKETCH_SMS 4
+#define SPIDGPU_OPT_SKETCH_PAIRS 5
 int spidgpu_set_option(spidgpu_handle h, int option, int64_t value);
 
 /* =====================================================================

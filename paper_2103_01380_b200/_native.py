@@ -23,6 +23,7 @@ SPIDGPU_OPT_GENERIC_CPQR = 1
 SPIDGPU_OPT_DMMA_SKETCH = 2
 SPIDGPU_OPT_IMMA_SKETCH = 3
 SPIDGPU_OPT_SKETCH_SMS = 4
+SPIDGPU_OPT_SKETCH_PAIRS = 5
 
 
 class SpidError(RuntimeError):

@@ -117,7 +117,7 @@ int do_sketch(spidgpu_handle h, Workspace& ws, const double* A, int64_t m, int64
         const int64_t ells = std::min<int64_t>(slice, ell - row0);
         SketchPlan plan;
         const int sms = h->sketch_sms > 0 ? h->sketch_sms : h->num_sms;
-        const bool planned = kind == K_TC ? sketch_tc_make_plan(m, n, batch, ells, sms, &plan)
+        const bool planned = kind == K_TC ? sketch_tc_make_plan(m, n, batch, ells, sms, h->sketch_pairs, &plan)
                              : kind == K_IMMA ? sketch_i8_make_plan(m, n, batch, ells, sms, &plan)
                                               : sketch_make_plan(m, n, batch, ells, sms, &plan);
         if (!planned) return fail(h, SPID_SHAPE_UNSUPPORTED, "no sketch plan");
@@ -590,6 +590,10 @@ int spidgpu_set_option(spidgpu_handle h, int option, int64_t value) {
         case SPIDGPU_OPT_GENERIC_CPQR: h->force_generic_cpqr = value != 0; return SPID_OK;
         case SPIDGPU_OPT_DMMA_SKETCH: h->force_dmma_sketch = value != 0; return SPID_OK;
         case SPIDGPU_OPT_IMMA_SKETCH: h->force_imma_sketch = value != 0; return SPID_OK;
+        case SPIDGPU_OPT_SKETCH_PAIRS:
+            if (value < 0 || value > 2) return SPID_INVALID_ARGUMENT;
+            h->sketch_pairs = static_cast<int>(value);
+            return SPID_OK;
         case SPIDGPU_OPT_SKETCH_SMS:
             if (value < 0) return SPID_INVALID_ARGUMENT;
             h->sketch_sms = static_cast<int>(std::min<int64_t>(value, h->num_sms));

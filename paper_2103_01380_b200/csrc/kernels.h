@@ -63,6 +63,8 @@ struct SketchPlan {
     int grid;             // CTAs (persistent, balanced contiguous ranges)
     int max_segs;         // partial slots per CTA
     int halves = 1;       // partial tiles per slot (2: the integer sketch's slice halves)
+    int pair = 0;         // 1: CTAs run as clusters of two over column-tile pairs (sketch_tc.cu);
+                          // total_chunks then counts pair units and grid stays the CTA count
     size_t smem;
     size_t partial_elems; // doubles of the partial workspace
 };
@@ -94,7 +96,7 @@ cudaError_t launch_sketch_i8(const SketchParams& p, const SketchPlan& plan, cons
                              cudaStream_t stream);
 // the same on tcgen05.mma kind::i8 with TMEM accumulators (sketch_tc.cu)
 constexpr int64_t kSketchTcMaxEll = 64;
-bool sketch_tc_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int num_sms,
+bool sketch_tc_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int num_sms, int pair_mode,
                          SketchPlan* plan);
 cudaError_t launch_sketch_tc(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap,
                              cudaStream_t stream);

@@ -242,22 +242,29 @@ __global__ void __launch_bounds__(kThreads, 1)
 constexpr int kRedRows = 8;
 constexpr int kRedMaxNt = 256;
 
+// pair = 1 (sketch_tc.cu CTA pairs): the stream-K units are (subdomain,
+// column-tile pair, stage) over G/2 pairs, and column tile ct was sketched by
+// CTA 2 * pair + ct % 2.
 __global__ void __launch_bounds__(256) sketch_reduce_kernel(SketchParams p, int ell_pad, int nt, int64_t nchunk,
                                      int64_t ntiles_col, int64_t total_chunks, int G,
-                                     int max_segs, int halves) {
+                                     int max_segs, int halves, int pair) {
     __shared__ double slab[kRedRows][kRedMaxNt + 1];
     __shared__ int cfirst, clast;
     const int nslab = (static_cast<int>(p.ell) + kRedRows - 1) / kRedRows;
     const int64_t tile = blockIdx.x / nslab;
     const int r0 = (blockIdx.x % nslab) * kRedRows;
     const int64_t s = tile / ntiles_col, ct = tile % ntiles_col;
-    const int64_t t0 = tile * nchunk, t1 = t0 + nchunk;
+    const int P = pair ? 2 : 1;
+    const int64_t utile = s * (ntiles_col / P) + ct / P;  // the work-unit tile
+    const int rk = static_cast<int>(ct % P);
+    const int Gu = G / P;
+    const int64_t t0 = utile * nchunk, t1 = t0 + nchunk;
     if (threadIdx.x == 0) {
-        int64_t cf = (t0 * G) / total_chunks;
-        while (cf > 0 && (cf * total_chunks) / G > t0) --cf;
-        while (((cf + 1) * total_chunks) / G <= t0) ++cf;
+        int64_t cf = (t0 * Gu) / total_chunks;
+        while (cf > 0 && (cf * total_chunks) / Gu > t0) --cf;
+        while (((cf + 1) * total_chunks) / Gu <= t0) ++cf;
         int64_t cl = cf;
-        while (cl + 1 < G && ((cl + 1) * total_chunks) / G < t1) ++cl;
+        while (cl + 1 < Gu && ((cl + 1) * total_chunks) / Gu < t1) ++cl;
         cfirst = static_cast<int>(cf);
         clast = static_cast<int>(cl);
     }
@@ -268,12 +275,13 @@ __global__ void __launch_bounds__(256) sketch_reduce_kernel(SketchParams p, int 
         const int rl = e / ncols, col = e % ncols;  // column fastest: coalesced partial reads
         double sum = 0.0;
         for (int cc = cfirst; cc <= clast; ++cc) {
-            const int64_t lo = (static_cast<int64_t>(cc) * total_chunks) / G;
-            const int64_t hi = (static_cast<int64_t>(cc + 1) * total_chunks) / G;
+            const int64_t lo = (static_cast<int64_t>(cc) * total_chunks) / Gu;
+            const int64_t hi = (static_cast<int64_t>(cc + 1) * total_chunks) / Gu;
             if (hi <= lo) continue;
-            const int segi = static_cast<int>(tile - lo / nchunk);
+            const int segi = static_cast<int>(utile - lo / nchunk);
+            const size_t cta = static_cast<size_t>(cc) * P + rk;
             for (int hv = 0; hv < halves; ++hv) {
-                const double* part = p.partial + ((static_cast<size_t>(cc) * max_segs + segi) * halves + hv) *
+                const double* part = p.partial + ((cta * max_segs + segi) * halves + hv) *
                                                      (static_cast<size_t>(ell_pad) * nt);
                 sum += part[(r0 + rl) * nt + col];
             }
@@ -416,7 +424,7 @@ cudaError_t launch_sketch_reduce(const SketchParams& p, const SketchPlan& plan, 
     const int nslab = static_cast<int>((p.ell + kRedRows - 1) / kRedRows);
     sketch_reduce_kernel<<<static_cast<unsigned>(p.batch * plan.ntiles_col * nslab), 256, 0, stream>>>(
         p, plan.ell_pad, plan.nt, plan.nchunk, plan.ntiles_col, plan.total_chunks, plan.grid,
-        plan.max_segs, plan.halves);
+        plan.max_segs, plan.halves, plan.pair);
     return cudaGetLastError();
 }
 

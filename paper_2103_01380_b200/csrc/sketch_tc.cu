@@ -149,6 +149,43 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                  : "memory");
 }
 
+// ---- CTA pairs (thread-block clusters of 2) ------------------------------------
+// completion of this CTA's MMAs arrives on the barrier at the same offset in both CTAs
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+            smem_u32(bar)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// the peer CTA's shared::cluster address of a local shared address
+__device__ __forceinline__ uint32_t peer_addr(uint32_t local, uint32_t peer) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(local), "r"(peer));
+    return r;
+}
+// 16 / 8 bytes into the peer's shared memory, completing on the peer's mbarrier
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                            uint32_t rbar) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];\n" ::"r"(raddr),
+        "r"(a), "r"(b), "r"(c), "r"(d), "r"(rbar)
+        : "memory");
+}
+__device__ __forceinline__ void st_async_v2(uint32_t raddr, uint32_t a, uint32_t b, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];\n" ::"r"(raddr),
+                 "r"(a), "r"(b), "r"(rbar)
+                 : "memory");
+}
+
 // .16x64b: the warp's 16 lanes from the address' lane field; thread t holds
 // lane 8 (t & 1) + (t >> 2), columns ((t >> 1) & 1) + 2 j (probed on B200:
 // tools/microbench/tmem_16dp.cu)
@@ -187,10 +224,20 @@ __device__ __forceinline__ double2 unfix_scale(int eb) {
                         __longlong_as_double(static_cast<long long>(e - e1 + 1023) << 52));
 }
 
-template <int NPAD>
+// kPair: the CTAs run as clusters of two that sketch the two column tiles
+// (128 snapshots each) of the same subdomain over the same 32-row stages, so
+// each generates HALF of every stage's Omega tile and writes it into both
+// CTAs' shared memory (the peer's half arrives by st.async, counted on the
+// local stage barrier as transaction bytes); every MMA completion is
+// multicast to both CTAs' slot barriers, so a slot is refilled only when
+// both CTAs' MMAs have read it. The stream-K partition runs over pair units
+// (subdomain, column-tile pair, stage); ntiles_u = column tiles per
+// subdomain / (1 + kPair).
+template <int NPAD, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchParams p, int64_t nchunk,
                      int64_t ntiles_col, int64_t total_chunks, int max_segs) {
+    constexpr int P = kPair ? 2 : 1;
     using Cfg = TcCfg<NPAD>;
     extern __shared__ unsigned char smem_raw[];
     const uint32_t raw_s = smem_u32(smem_raw);
@@ -208,10 +255,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* b_empty = b_full + kBStages;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t G = gridDim.x, c = blockIdx.x;
-    const int64_t lo = (c * total_chunks) / G, hi = ((c + 1) * total_chunks) / G;
+    const int64_t c = blockIdx.x;
+    const uint32_t rank = kPair ? cluster_ctarank() : 0u;
+    const int64_t G = gridDim.x / P, cu = c / P;  // work-unit owners: CTAs, or CTA pairs
+    const int64_t lo = (cu * total_chunks) / G, hi = ((cu + 1) * total_chunks) / G;
     const int niter = static_cast<int>(hi - lo);
-    if (niter <= 0) return;
+    if (niter <= 0) return;  // both CTAs of a pair share the range
 
     for (int i = tid; i < 1024; i += kThreads)
         reinterpret_cast<int*>(tab)[i] = reinterpret_cast<const int*>(kOmegaQ)[i];
@@ -225,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < kBStages; ++i) {
             mbar_init(&b_full[i], kConvWarps + kGenWarps);
-            mbar_init(&b_empty[i], 1);
+            mbar_init(&b_empty[i], P);  // MMA commits of this CTA (and of its peer)
         }
         fence_barrier_init();
     }
@@ -235,7 +284,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (kPair)
+        cluster_sync_all();  // barriers initialised in both CTAs before any remote traffic
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -248,11 +300,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         // (8 entries of one Omega row, an 8-byte store) when the tile has at
         // most one per generator lane, else two (16 bytes): each lane runs at
         // most one task per stage, so the tile's latency is one task's.
-        constexpr bool kFine = 4 * NPAD <= 32 * kGenWarps;
+        // A pair splits the tile's tasks: this CTA runs [rank, rank + 1) x
+        // kTasksCta of them and also writes them into the peer's tile.
+        constexpr bool kFine = 4 * NPAD <= 32 * kGenWarps * P;
         constexpr int kTasks = kFine ? 4 * NPAD : 2 * NPAD;
-        constexpr int kTasksPerWarp = (kTasks + kGenWarps - 1) / kGenWarps;
+        constexpr int kTasksCta = kTasks / P;
+        constexpr int kTasksPerWarp = (kTasksCta + kGenWarps - 1) / kGenWarps;
+        constexpr uint32_t kPeerBytes = kTasksCta * (kFine ? 8 : 16);  // Omega bytes the peer sends per stage
         static_assert(kTasksPerWarp <= 32, "one Omega task per lane");
         const int gw = warp == 0 ? 0 : warp - 1;
+        const uint32_t peer = rank ^ 1u;
 
         constexpr uint32_t kIdU = idesc_i8(NPAD, false);
         const uint64_t ones_desc = smem_desc(ones_s, 0, 0);
@@ -267,7 +324,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int t = 0; t < kSlices; ++t)
                 umma_i8(tmem + NPAD * t, smem_desc(st + t * kSliceBytes, kM * 16, 128), bdesc, kIdU, acc);
             umma_i8(tmem + NPAD * kSlices, ones_desc, bdesc, kIdU, acc);
-            umma_commit(&b_empty[sl]);
+            if constexpr (kPair)
+                umma_commit_pair(&b_empty[sl]);
+            else
+                umma_commit(&b_empty[sl]);
         };
         ChunkPos cp = chunk_pos(lo, nchunk, ntiles_col);
         ChunkPos tp = cp;  // TMA position (warp 0)
@@ -277,7 +337,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int b = 0; b < 2; ++b)
                 tma_load_3d(base + sl * kAStageBytes + b * kBoxBytes, &tmap, &a_full[sl],
-                            static_cast<int>(tp.kc * kRows + 16 * b), static_cast<int>(tp.ct * kM),
+                            static_cast<int>(tp.kc * kRows + 16 * b),
+                            static_cast<int>((tp.ct * P + static_cast<int>(rank)) * kM),
                             static_cast<int>(tp.s));
             advance(tp, static_cast<int>(nchunk), static_cast<int>(ntiles_col));
         };
@@ -291,8 +352,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int sl = it % kBStages;
             const uint32_t ot = b_s + sl * Cfg::kBStageBytes + kSlices * kSliceBytes;
             const uint32_t ko = static_cast<uint32_t>((cp.kc * kRows) >> 3);
-            const int task = gw * kTasksPerWarp + lane;
-            const bool has_task = lane < kTasksPerWarp && task < kTasks;
+            const int task_l = gw * kTasksPerWarp + lane;
+            const bool has_task = lane < kTasksPerWarp && task_l < kTasksCta;
+            const int task = static_cast<int>(rank) * kTasksCta + task_l;
             // row r, K octet(s) from o8: fine tasks one octet, else a 16-byte K half
             const int r = task % NPAD, o8 = (kFine ? 1 : 2) * (task / NPAD);
             constexpr int kOct = kFine ? 1 : 2;
@@ -318,10 +380,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                     sts64u(dst, w[0], w[1]);
                 else
                     sts128u(dst, w[0], w[1], w[2 * kOct - 2], w[2 * kOct - 1]);
+                if constexpr (kPair) {  // the peer's copy, counted on its stage barrier
+                    const uint32_t rdst = peer_addr(dst, peer), rbar = peer_addr(smem_u32(&b_full[sl]), peer);
+                    if constexpr (kFine)
+                        st_async_v2(rdst, w[0], w[1], rbar);
+                    else
+                        st_async_v4(rdst, w[0], w[1], w[2 * kOct - 2], w[2 * kOct - 1], rbar);
+                }
             }
             fence_proxy_async();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&b_full[sl]);
+            if (lane == 0) {
+                if (kPair && warp == 0)
+                    mbar_arrive_expect_tx(&b_full[sl], kPeerBytes);  // the peer's half of the tile
+                else
+                    mbar_arrive(&b_full[sl]);
+            }
             advance(cp, static_cast<int>(nchunk), static_cast<int>(ntiles_col));
             if (lane == 0) {
                 if (warp == 0 && it + kAStages < niter) {
@@ -525,30 +599,90 @@ __global__ void __launch_bounds__(kThreads, 1)
         // final flush of the last segment
         flush(niter - 1, true, false);
     }
-    __syncthreads();
+    if constexpr (kPair)
+        cluster_sync_all();  // no remote store or commit may target a CTA that has exited
+    else
+        __syncthreads();
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(Cfg::kTmemCols));
     }
 }
 
-template <int NPAD>
+template <int NPAD, bool kPair>
 cudaError_t launch_t(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap, cudaStream_t stream) {
     using Cfg = TcCfg<NPAD>;
     static_assert(Cfg::kSmem <= 227 * 1024, "shared memory budget");
-    auto kern = sketch_tc_kernel<NPAD>;
+    auto kern = sketch_tc_kernel<NPAD, kPair>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::kSmem));
     if (e != cudaSuccess) return e;
-    kern<<<plan.grid, kThreads, Cfg::kSmem, stream>>>(*tmap, p, plan.nchunk, plan.ntiles_col, plan.total_chunks,
-                                                      plan.max_segs);
-    e = cudaGetLastError();
+    const int64_t ntiles_u = plan.ntiles_col / (kPair ? 2 : 1);
+    if constexpr (kPair) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(plan.grid));
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = Cfg::kSmem;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, kern, *tmap, p, plan.nchunk, ntiles_u, plan.total_chunks, plan.max_segs);
+    } else {
+        kern<<<plan.grid, kThreads, Cfg::kSmem, stream>>>(*tmap, p, plan.nchunk, ntiles_u, plan.total_chunks,
+                                                          plan.max_segs);
+        e = cudaGetLastError();
+    }
     if (e != cudaSuccess) return e;
     return launch_sketch_reduce(p, plan, stream);
 }
 
+// CTA pairs the device keeps resident at once for this kernel (0 if clusters
+// of two cannot be launched); cached per ell_pad
+template <int NPAD>
+int max_pairs() {
+    static int cached = -1;
+    if (cached >= 0) return cached;
+    using Cfg = TcCfg<NPAD>;
+    auto kern = sketch_tc_kernel<NPAD, true>;
+    int n = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::kSmem)) ==
+        cudaSuccess) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = Cfg::kSmem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) n = 0;
+    }
+    cudaGetLastError();
+    cached = n;
+    return n;
+}
+
+int max_pairs_for(int ell_pad) {
+    switch (ell_pad) {
+        case 16: return max_pairs<16>();
+        case 32: return max_pairs<32>();
+        case 48: return max_pairs<48>();
+        case 64: return max_pairs<64>();
+        default: return 0;
+    }
+}
+
 }  // namespace
 
-bool sketch_tc_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int num_sms, SketchPlan* plan) {
+bool sketch_tc_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int num_sms, int pair_mode,
+                         SketchPlan* plan) {
     if (m < 1 || n < 1 || batch < 1 || ell < 1 || ell > kSketchTcMaxEll) return false;
     plan->ell_pad = static_cast<int>(16 * ((ell + 15) / 16));
     plan->mt = plan->ell_pad / 16;
@@ -557,25 +691,43 @@ bool sketch_tc_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int n
     plan->ntiles_col = (n + kM - 1) / kM;
     plan->kc_rows = kRows;
     plan->nchunk = (m + kRows - 1) / kRows;
-    plan->total_chunks = batch * plan->ntiles_col * plan->nchunk;
-    int64_t grid = num_sms;
-    if (grid > plan->total_chunks) grid = plan->total_chunks;
-    plan->grid = static_cast<int>(grid);
-    const int64_t per = (plan->total_chunks + grid - 1) / grid;
+    // CTA pairs when the column tiles pair up and the device keeps at least
+    // as many pairs resident as half the SM budget (clusters of two span a
+    // TPC). pair_mode 1 (default) pairs only ell_pad 64, where halving the
+    // Omega work outweighs the pair's lock-step (base clock, config 3: -3% at
+    // 64, +4.5% at 48, +8% at 16); 2 pairs whenever possible (tests, A/B).
+    const bool want = pair_mode == 2 || (pair_mode == 1 && plan->ell_pad == 64);
+    const int pairs = want && num_sms >= 2 && plan->ntiles_col % 2 == 0 ? max_pairs_for(plan->ell_pad) : 0;
+    plan->pair = pairs > 0 && 2 * pairs >= num_sms - 1 ? 1 : 0;
+    const int P = plan->pair ? 2 : 1;
+    plan->total_chunks = batch * (plan->ntiles_col / P) * plan->nchunk;  // work units
+    int64_t owners = plan->pair ? std::min<int64_t>(pairs, num_sms / 2) : num_sms;
+    if (owners > plan->total_chunks) owners = plan->total_chunks;
+    plan->grid = static_cast<int>(owners * P);
+    const int64_t per = (plan->total_chunks + owners - 1) / owners;
     plan->max_segs = static_cast<int>(per / plan->nchunk + 2);
     plan->smem = 0;
-    plan->partial_elems = static_cast<size_t>(grid) * plan->max_segs * plan->ell_pad * plan->nt;
+    plan->partial_elems = static_cast<size_t>(plan->grid) * plan->max_segs * plan->ell_pad * plan->nt;
     return true;
 }
 
 cudaError_t launch_sketch_tc(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap,
                              cudaStream_t stream) {
     if (p.omega_mode != 1) return cudaErrorInvalidValue;
+    if (plan.pair) {
+        switch (plan.ell_pad) {
+            case 16: return launch_t<16, true>(p, plan, tmap, stream);
+            case 32: return launch_t<32, true>(p, plan, tmap, stream);
+            case 48: return launch_t<48, true>(p, plan, tmap, stream);
+            case 64: return launch_t<64, true>(p, plan, tmap, stream);
+            default: return cudaErrorInvalidValue;
+        }
+    }
     switch (plan.ell_pad) {
-        case 16: return launch_t<16>(p, plan, tmap, stream);
-        case 32: return launch_t<32>(p, plan, tmap, stream);
-        case 48: return launch_t<48>(p, plan, tmap, stream);
-        case 64: return launch_t<64>(p, plan, tmap, stream);
+        case 16: return launch_t<16, false>(p, plan, tmap, stream);
+        case 32: return launch_t<32, false>(p, plan, tmap, stream);
+        case 48: return launch_t<48, false>(p, plan, tmap, stream);
+        case 64: return launch_t<64, false>(p, plan, tmap, stream);
         default: return cudaErrorInvalidValue;
     }
 }

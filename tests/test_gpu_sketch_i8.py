@@ -2,8 +2,9 @@
 Y = Omega A with Omega = Q/32 integer-valued, A split into 7 byte slices of a
 55-bit per-column fixed point, each slice contracted exactly in int32 --
 on tcgen05.mma kind::i8 with TMEM accumulators (csrc/sketch_tc.cu, the
-default) and on register-fed IMMA.16832 (csrc/sketch_i8.cu,
-SPIDGPU_OPT_IMMA_SKETCH). Every test runs on both kernels.
+default; also forced into its CTA-pair mode, which shares each stage's Omega
+tile between the two CTAs of a cluster) and on register-fed IMMA.16832
+(csrc/sketch_i8.cu, SPIDGPU_OPT_IMMA_SKETCH). Every test runs on all three.
 
 Checked against the oracle's matmul (proj/src/dense_matrix.cpp:38-53) on the
 materialised Omega, and against the FP64 DMMA kernel (SPIDGPU_OPT_DMMA_SKETCH)
@@ -28,15 +29,20 @@ def _dmma(engine, on):
     engine.h.check(N.lib.spidgpu_set_option(engine.h.h, N.SPIDGPU_OPT_DMMA_SKETCH, int(on)))
 
 
-@pytest.fixture(params=["tc", "imma"], autouse=True)
+@pytest.fixture(params=["tc", "tc_pairs", "imma"], autouse=True)
 def kernel(request, engine):
-    """Route the Philox sketches of the shared engine to one kernel."""
+    """Route the Philox sketches of the shared engine to one kernel: tcgen05
+    (CTA pairs only for 64-row passes, the default), tcgen05 with CTA pairs
+    wherever the column tiles pair up, or register-fed IMMA."""
     from paper_2103_01380_b200 import _native as N
 
     engine.h.check(N.lib.spidgpu_set_option(engine.h.h, N.SPIDGPU_OPT_IMMA_SKETCH,
                                             int(request.param == "imma")))
+    engine.h.check(N.lib.spidgpu_set_option(engine.h.h, N.SPIDGPU_OPT_SKETCH_PAIRS,
+                                            2 if request.param == "tc_pairs" else 1))
     yield request.param
     engine.h.check(N.lib.spidgpu_set_option(engine.h.h, N.SPIDGPU_OPT_IMMA_SKETCH, 0))
+    engine.h.check(N.lib.spidgpu_set_option(engine.h.h, N.SPIDGPU_OPT_SKETCH_PAIRS, 1))
 
 
 def _check_vs_oracle(engine, spid, orc, A, ell, seed, base, tol=1e-13):
@@ -69,7 +75,8 @@ def test_omega_is_the_discretised_gaussian(spid):
 
 @pytest.mark.parametrize("m,n,ell", [(6000, 130, 48), (16384, 100, 20), (1000, 37, 30),
                                      (2048, 512, 16), (18, 7, 3), (34, 65, 33), (1026, 129, 47),
-                                     (100, 257, 1), (5000, 64, 80), (3000, 70, 100)])
+                                     (100, 257, 1), (5000, 64, 80), (3000, 70, 100), (4000, 256, 64),
+                                     (3500, 384, 60)])
 def test_i8_sketch_matches_oracle(engine, spid, orc, m, n, ell):
     torch.manual_seed(m + n + ell)
     A = torch.randn((3, n, m), dtype=torch.float64, device="cuda")
