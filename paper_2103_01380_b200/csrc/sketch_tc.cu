@@ -641,7 +641,8 @@ cudaError_t launch_t(const SketchParams& p, const SketchPlan& plan, const CUtens
 }
 
 // CTA pairs the device keeps resident at once for this kernel (0 if clusters
-// of two cannot be launched); cached per ell_pad
+// of two cannot be launched); cached per ell_pad for the process's device
+// (one GPU per process; a racing first call computes the same value)
 template <int NPAD>
 int max_pairs() {
     static int cached = -1;

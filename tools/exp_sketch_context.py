@@ -1,23 +1,39 @@
-import sys, torch
-sys.path.insert(0, '/root/repo')
-from paper_2103_01380_b200.configs import CONFIGS
-from paper_2103_01380_b200.engine import Engine, rule_for
-cfg = CONFIGS['cfg3']; big = CONFIGS['cfg5']
-eng = Engine(0); A = eng.generate(big, 0, 64); rule = rule_for(cfg)
-r = eng.compress(A, cfg.ell, rule, seed=cfg.seed, want_sketch=True); r.check()
+"""Sketch duration inside the compress step vs back-to-back alone (config 3,
+CUDA events on the launching stream). python tools/exp_sketch_context.py"""
+import sys
+
+import torch
+
+sys.path.insert(0, "/root/repo")
+import bench  # noqa: E402
+from paper_2103_01380_b200.engine import Engine, rule_for  # noqa: E402
+
+cfg, field, first, count = bench.workload("cfg3", 0, 1)
+eng = Engine(0)
+A = eng.generate(field, first, count)
+rule = rule_for(cfg)
+res = eng.compress(A, cfg.ell, rule, seed=cfg.seed, want_sketch=True)
+torch.cuda.synchronize()
 st = torch.cuda.current_stream()
-def ev(): return torch.cuda.Event(enable_timing=True)
-def run(mode, reps=6):
-    ts = []
-    for i in range(reps):
-        if mode == 'after_gather': eng.gather(A, r)
-        if mode == 'after_cpqr': eng.cpqr(r.sketch, rule)
-        if mode == 'after_flush':
-            buf = torch.empty(256 * 2**20, dtype=torch.uint8, device='cuda'); buf.fill_(1)
-        a, b = ev(), ev(); a.record(st)
-        eng.sketch(A, cfg.ell, seed=cfg.seed, out=r.sketch)
-        b.record(st); ts.append((a, b))
+
+
+def run(mode, reps=20):
+    ev = []
+    for i in range(reps + 3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        eng.sketch(A, cfg.ell, seed=cfg.seed, out=res.sketch)
+        b.record(st)
+        if i >= 3:
+            ev.append((a, b))
+        if mode == "step":
+            eng.h.check(bench._cpqr_into(eng, res, rule))
+            eng.h.check(bench._gather_into(eng, A, res))
     torch.cuda.synchronize()
-    v = [x.elapsed_time(y) for x, y in ts][1:]
-    print(mode, ['%.3f' % t for t in v])
-for m in ['alone', 'after_gather', 'after_cpqr', 'after_flush', 'alone']: run(m)
+    t = sorted(a.elapsed_time(b) for a, b in ev)
+    return t[len(t) // 2], t[0], t[-1]
+
+
+for mode in ["alone", "step", "alone", "step"]:
+    med, lo, hi = run(mode)
+    print(f"{mode:5s}: sketch median {med:.3f} ms (min {lo:.3f}, max {hi:.3f})", flush=True)
