@@ -55,7 +55,13 @@ struct spidgpu_stream {
     cudaEvent_t ready = nullptr, free_ev[2] = {nullptr, nullptr};
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> s1_events;
     Workspace ws_cmp, ws_fin;
-    DevBuf staging;
+    // host frames land in alternating staging buffers: the gather of one push
+    // (same stream, so ordered before the buffer's next copy) overlaps the
+    // next push's copy; a push returns once its own copy has read the host data
+    DevBuf staging[2];
+    int64_t staged[2] = {0, 0};  // entries each staging buffer holds
+    cudaEvent_t copied = nullptr;
+    int stg = 0;
     int64_t filled = 0, snapshots = 0, nchunks = 0, stage1_tasks = 0, stage2_tasks = 0;
     int64_t fine_peak = 0, coarse_peak = 0;
     double stage2_ms = 0.0;
@@ -155,7 +161,9 @@ void destroy(spidgpu_stream* s) {
     }
     s->ws_cmp.release();
     s->ws_fin.release();
-    s->staging.release();
+    s->staging[0].release();
+    s->staging[1].release();
+    if (s->copied) cudaEventDestroy(s->copied);
     for (auto& e : s->s1_events) {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
@@ -210,7 +218,8 @@ int spidgpu_stream_open(spidgpu_handle h, const spidgpu_stream_config* cfg, spid
         cudaStreamCreateWithFlags(&s->s_cmp, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&s->ready, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&s->free_ev[0], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&s->free_ev[1], cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&s->free_ev[1], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->copied, cudaEventDisableTiming) != cudaSuccess)
         return bail(fail(h, SPID_CUDA_ERROR, "stream/event creation failed"));
     for (const Group& G : group_blocks(s->L, nullptr)) {
         SGroup g;
@@ -254,12 +263,16 @@ int spidgpu_stream_push(spidgpu_stream_handle s, const double* frames, int64_t m
         const double* src = frames + j * ld;
         int64_t lds = ld;
         if (!on_device) {  // stage the frames (the only fine-grid data the stream holds)
-            SCK(s, s->staging.ensure(sizeof(double) * m * c, s->s_in));
-            SCK(s, cudaMemcpy2DAsync(s->staging.ptr, sizeof(double) * m, src, sizeof(double) * ld,
+            DevBuf& sb = s->staging[s->stg];
+            s->staged[s->stg] = m * c;
+            s->stg ^= 1;
+            SCK(s, sb.ensure(sizeof(double) * m * c, s->s_in));
+            SCK(s, cudaMemcpy2DAsync(sb.ptr, sizeof(double) * m, src, sizeof(double) * ld,
                                      sizeof(double) * m, c, cudaMemcpyHostToDevice, s->s_in));
-            src = s->staging.as<double>();
+            SCK(s, cudaEventRecord(s->copied, s->s_in));
+            src = sb.as<double>();
             lds = m;
-            s->fine_peak = std::max(s->fine_peak, m * c);
+            s->fine_peak = std::max(s->fine_peak, s->staged[0] + s->staged[1]);
         }
         if (s->filled == 0 && s->groups[0].used[s->cur])  // <= 2 chunks in flight
             SCK(s, cudaStreamWaitEvent(s->s_in, s->free_ev[s->cur], 0));
@@ -277,7 +290,7 @@ int spidgpu_stream_push(spidgpu_stream_handle s, const double* frames, int64_t m
             if (rc) return rc;
         }
     }
-    if (!on_device) SCK(s, cudaStreamSynchronize(s->s_in));  // staging reused by the next push
+    if (!on_device) SCK(s, cudaEventSynchronize(s->copied));  // the host frames have been read
     return SPID_OK;
 }
 
