@@ -396,30 +396,34 @@ __global__ void __launch_bounds__(kMode == 2 ? kCpqrThreads + kWarp : kCpqrThrea
             start_sweeps(3);
             double r1 = 0.0, r2 = 0.0, nn = 0.0;
             double* Wj = W + j;
-            // rows of a chunk in order: whole groups of 8 with the next group's
-            // (q, w) loaded before the current group's dependent chain (the
-            // last group reloads itself, branch-free), then the ragged tail
+            // rows of a chunk in order: whole groups of kGrp with the next
+            // group's (q, w) loaded before the current group's dependent chain
+            // (the last group reloads itself, branch-free), then the ragged tail
+            // 16-row groups for narrow W (one or two column warps, latency-bound
+            // chains: 4096 x 32 batch 3.04 -> 2.85 ms), 8 for wide (4096 x 256:
+            // 15.2 vs 17.0 ms with 16)
+            constexpr int kGrp = (kNpad != 0 && kNpad <= 64) ? 16 : 8;
             auto rows = [&](const double* ck, int nr, auto&& f) {
-                const int nfull = nr & ~7;
+                const int nfull = nr & ~(kGrp - 1);
                 if (nfull) {
-                    double qa[8], wa[8];
+                    double qa[kGrp], wa[kGrp];
 #pragma unroll
-                    for (int t = 0; t < 8; ++t) {
+                    for (int t = 0; t < kGrp; ++t) {
                         qa[t] = ck[t * npad + pc];
                         wa[t] = ck[t * npad + j];
                     }
-                    for (int u0 = 0; u0 < nfull; u0 += 8) {
-                        const int un = min(u0 + 8, nfull - 8);
-                        double qb[8], wb[8];
+                    for (int u0 = 0; u0 < nfull; u0 += kGrp) {
+                        const int un = min(u0 + kGrp, nfull - kGrp);
+                        double qb[kGrp], wb[kGrp];
 #pragma unroll
-                        for (int t = 0; t < 8; ++t) {
+                        for (int t = 0; t < kGrp; ++t) {
                             qb[t] = ck[(un + t) * npad + pc];
                             wb[t] = ck[(un + t) * npad + j];
                         }
 #pragma unroll
-                        for (int t = 0; t < 8; ++t) f(u0 + t, qa[t], wa[t]);
+                        for (int t = 0; t < kGrp; ++t) f(u0 + t, qa[t], wa[t]);
 #pragma unroll
-                        for (int t = 0; t < 8; ++t) {
+                        for (int t = 0; t < kGrp; ++t) {
                             qa[t] = qb[t];
                             wa[t] = wb[t];
                         }
