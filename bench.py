@@ -218,7 +218,7 @@ def run_reference(args):
         "data": "synthetic",
         "config": {"workload": f"{cfg.name}: bounded sample of {nsamp} subdomains of "
                               f"{cfg.m}x{cfg.n} (k={cfg.k}, p={cfg.p}) on {threads} host threads",
-                   "global_batch": nsamp, "seq_len": cfg.n, "parallelism": "cpu-threads"},
+                   "subdomains": nsamp, "snapshots": cfg.n, "partition": "one subdomain per host thread"},
         "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -397,7 +397,8 @@ def run_ours(args):
                                   f"global blocks [64r, 64r+64) on rank r (rank 0: [{first}, {first + count}))")
                                + f" of "
                                f"the {field.grid}^3 multimode TGV field",
-                   "global_batch": count * world, "seq_len": cfg.n, "parallelism": f"dp{world}",
+                   "subdomains": count * world, "snapshots": cfg.n,
+                   "partition": f"static subdomain ranges over {world} GPU(s), no data exchange",
                    "l2": "inputs (21.5 GB/GPU) larger than L2 (126 MB); no flush needed"},
         "cf": report.cf, "rel_frob_error": report.rel_frob_error,
         "stored_entries": report.stored_entries,
