@@ -398,7 +398,8 @@ def run_ours(args):
                                + f" of "
                                f"the {field.grid}^3 multimode TGV field",
                    "subdomains": count * world, "snapshots": cfg.n,
-                   "partition": f"static subdomain ranges over {world} GPU(s), no data exchange",
+                   "partition": (f"subdomains dealt round-robin over {world} GPU(s)" if cfg.adaptive else
+                                 f"static subdomain ranges over {world} GPU(s)") + ", no data exchange",
                    "l2": "inputs (21.5 GB/GPU) larger than L2 (126 MB); no flush needed"},
         "cf": report.cf, "rel_frob_error": report.rel_frob_error,
         "stored_entries": report.stored_entries,
