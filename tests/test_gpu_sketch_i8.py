@@ -157,6 +157,8 @@ def test_i8_sketch_sm_cap(engine, spid, orc, sms):
     finally:
         engine.h.check(N.lib.spidgpu_set_option(engine.h.h, N.SPIDGPU_OPT_SKETCH_SMS, 0))
     assert N.lib.spidgpu_set_option(engine.h.h, N.SPIDGPU_OPT_SKETCH_SMS, -1) != 0
+    for bad in (-1, 3):
+        assert N.lib.spidgpu_set_option(engine.h.h, N.SPIDGPU_OPT_SKETCH_PAIRS, bad) != 0
 
 
 def test_i8_large_subdomain_cfg3_shape(engine, spid, orc):
