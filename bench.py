@@ -337,7 +337,7 @@ def run_ours(args):
     verify_ms = float(vt[0])
 
     # roofline of the dominant kernel (the sketch). The Philox-Omega sketch
-    # is the exact integer-sliced contraction (sketch_i8.cu): it reads A once
+    # is the exact integer-sliced contraction (sketch_tc.cu): it reads A once
     # and is bound by HBM; the FP64-equivalent flop rate is reported beside
     # it against the DMMA roofline the FP64 kernel was bound by.
     flops = 2.0 * cfg.ell * cfg.m * cfg.n * count
@@ -364,11 +364,11 @@ def run_ours(args):
     }
 
     # A/B evidence for the sketch design: the same Philox sketch on the FP64
-    # DMMA kernel and on the register-fed IMMA variant (identical Omega)
+    # DMMA kernel (identical Omega)
     from paper_2103_01380_b200 import _native as NN
 
     variants = {}
-    for vname, opt in (("dmma_fp64", NN.SPIDGPU_OPT_DMMA_SKETCH), ("imma_mma_sync", NN.SPIDGPU_OPT_IMMA_SKETCH)):
+    for vname, opt in (("dmma_fp64", NN.SPIDGPU_OPT_DMMA_SKETCH),):
         eng.h.check(NN.lib.spidgpu_set_option(eng.h.h, opt, 1))
         try:
             eng.sketch(A, cfg.ell, seed=cfg.seed, subdomain_base=first, out=res.sketch)

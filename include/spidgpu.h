@@ -85,22 +85,33 @@ int64_t spidgpu_launch_count(spidgpu_handle h);
  * kernel instead of the register-resident one; both are bit-exact with the
  * reference, the option exists so tests can cover both.
  * SPIDGPU_OPT_DMMA_SKETCH = 2 runs Philox-Omega sketches on the FP64 DMMA
- * kernel, SPIDGPU_OPT_IMMA_SKETCH = 3 on the register-fed IMMA variant of
- * the exact integer-sliced contraction, instead of its tcgen05 (TMEM) kernel
- * (same Omega; the options exist for tests and A/B measurement).
+ * kernel instead of the exact integer-sliced tcgen05 (TMEM) kernel (same
+ * Omega; the option exists for tests and A/B measurement). Option 3 (a
+ * retired register-fed IMMA variant) is rejected.
  * SPIDGPU_OPT_SKETCH_SMS = 4 caps the SMs the persistent sketch kernels
  * occupy (0 = all), leaving the rest to kernels on other streams (the
  * overlapped compress pipeline).
  * SPIDGPU_OPT_SKETCH_PAIRS = 5 runs the tcgen05 sketch as clusters of two
  * CTAs that share each stage's Omega tile: 0 never, 1 (default) where it
- * measured faster (64-row passes), 2 whenever the column tiles pair up (same
- * results to the parity bound; tests and A/B). */
+ * measured faster (64-row passes), 2 whenever the column tiles pair up
+ * (bitwise the same Y; tests and A/B).
+ * Every sketch is bitwise independent of the batch it runs in, the SM cap,
+ * the pair mode and the GPU count: work is split at fixed 4096-row segment
+ * boundaries and segment partials are summed in a fixed order.
+ * SPIDGPU_OPT_SKETCH_SEG_ROWS = 6 sets the tcgen05 sketch's segment length in
+ * rows (0 = the default 4096; a multiple of 512 up to 65536). Results are
+ * independent of batching for any fixed value, but differ (within the
+ * accuracy contract) between values; the option exists for measurement. */
 #define SPIDGPU_OPT_GENERIC_CPQR 1
 #define SPIDGPU_OPT_DMMA_SKETCH 2
-#define SPIDGPU_OPT_IMMA_SKETCH 3
 #define SPIDGPU_OPT_SKETCH_SMS 4
 #define SPIDGPU_OPT_SKETCH_PAIRS 5
+#define SPIDGPU_OPT_SKETCH_SEG_ROWS 6
 int spidgpu_set_option(spidgpu_handle h, int option, int64_t value);
+/* Instrumentation: out[0..2] = tcgen05-sketch converter-warp flushes since
+ * the last reset, by cause (segment end, exponent-headroom overflow,
+ * magnitude fallback); process-wide for the handle's device. n >= 3. */
+int spidgpu_debug_counters(spidgpu_handle h, int64_t* out, int n, int reset);
 
 /* =====================================================================
  * Batched device API (the hot path). Subdomain s of a batch lives at

@@ -21,9 +21,9 @@ OMEGA_EXPLICIT, OMEGA_PHILOX = 0, 1
 FIELD_TGV4, FIELD_TGV5, FIELD_MULTIMODE = 0, 1, 2
 SPIDGPU_OPT_GENERIC_CPQR = 1
 SPIDGPU_OPT_DMMA_SKETCH = 2
-SPIDGPU_OPT_IMMA_SKETCH = 3
 SPIDGPU_OPT_SKETCH_SMS = 4
 SPIDGPU_OPT_SKETCH_PAIRS = 5
+SPIDGPU_OPT_SKETCH_SEG_ROWS = 6
 
 
 class SpidError(RuntimeError):
@@ -120,6 +120,7 @@ _SIGS = {
     "spidgpu_abi_version": (C.c_int, []),
     "spidgpu_launch_count": (C.c_int64, [_H]),
     "spidgpu_set_option": (C.c_int, [_H, C.c_int, C.c_int64]),
+    "spidgpu_debug_counters": (C.c_int, [_H, C.POINTER(C.c_int64), C.c_int, C.c_int]),
     "spidgpu_sketch_batched": (C.c_int, [_H, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _OM, _vp,
                                          _i64, _i64, _vp]),
     "spidgpu_philox_omega": (C.c_int, [_H, C.c_uint64, _i64, _i64, _i64, _vp, _i64, _vp]),
@@ -185,6 +186,8 @@ def _load():
                           " (there is no CPU fallback)")
     lib = C.CDLL(LIB_PATH)
     for name, (res, args) in _SIGS.items():
+        if os.environ.get("SPIDGPU_LIB_PATH") and not hasattr(lib, name):
+            continue  # an older A/B build may predate newer entry points
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

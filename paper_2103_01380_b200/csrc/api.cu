@@ -100,14 +100,11 @@ int do_sketch(spidgpu_handle h, Workspace& ws, const double* A, int64_t m, int64
     if (om->mode == SPIDGPU_OMEGA_EXPLICIT && om->ldo < ell)
         return fail(h, SPID_INVALID_ARGUMENT, "ldo < ell");
     // Philox Omega: exact integer-sliced contraction on tcgen05 (UTCIMMA,
-    // HBM-bound), or on register-fed IMMA (SPIDGPU_OPT_IMMA_SKETCH); explicit
-    // Omega (arbitrary fp64 entries) and SPIDGPU_OPT_DMMA_SKETCH: the DMMA kernel
-    enum { K_DMMA, K_IMMA, K_TC };
-    const int kind = om->mode != SPIDGPU_OMEGA_PHILOX || h->force_dmma_sketch ? K_DMMA
-                     : h->force_imma_sketch                                  ? K_IMMA
-                                                                             : K_TC;
-    int64_t slice = kind == K_TC ? kSketchTcMaxEll : kind == K_IMMA ? kSketchI8MaxEll : 80;
-    if (kind == K_TC && ell > slice) {
+    // HBM-bound); explicit Omega (arbitrary fp64 entries) and
+    // SPIDGPU_OPT_DMMA_SKETCH: the DMMA kernel
+    const bool tc = om->mode == SPIDGPU_OMEGA_PHILOX && !h->force_dmma_sketch;
+    int64_t slice = tc ? kSketchTcMaxEll : 80;
+    if (tc && ell > slice) {
         // even passes of whole 16-row groups: ell = 80 runs as 48 + 32, not 64 + 16
         // (the Omega/MMA work per A pass grows with the pass width)
         const int64_t passes = (ell + slice - 1) / slice;
@@ -117,9 +114,8 @@ int do_sketch(spidgpu_handle h, Workspace& ws, const double* A, int64_t m, int64
         const int64_t ells = std::min<int64_t>(slice, ell - row0);
         SketchPlan plan;
         const int sms = h->sketch_sms > 0 ? h->sketch_sms : h->num_sms;
-        const bool planned = kind == K_TC ? sketch_tc_make_plan(m, n, batch, ells, sms, h->sketch_pairs, &plan)
-                             : kind == K_IMMA ? sketch_i8_make_plan(m, n, batch, ells, sms, &plan)
-                                              : sketch_make_plan(m, n, batch, ells, sms, &plan);
+        const bool planned = tc ? sketch_tc_make_plan(m, n, batch, ells, sms, h->sketch_pairs, h->sketch_seg_rows, &plan)
+                                : sketch_make_plan(m, n, batch, ells, sms, &plan);
         if (!planned) return fail(h, SPID_SHAPE_UNSUPPORTED, "no sketch plan");
         CK(h, ws.partial.ensure(plan.partial_elems * sizeof(double), st));
         CUtensorMap tmap;
@@ -154,9 +150,7 @@ int do_sketch(spidgpu_handle h, Workspace& ws, const double* A, int64_t m, int64
         p.Y = Y;
         p.ldy = ldy;
         p.strideY = strideY;
-        CK(h, kind == K_TC ? launch_sketch_tc(p, plan, &tmap, st)
-              : kind == K_IMMA ? launch_sketch_i8(p, plan, &tmap, st)
-                               : launch_sketch(p, plan, &tmap, st));
+        CK(h, tc ? launch_sketch_tc(p, plan, &tmap, st) : launch_sketch(p, plan, &tmap, st));
         h->launches += 2;
     }
     return SPID_OK;
@@ -580,6 +574,13 @@ int spidgpu_destroy(spidgpu_handle h) {
     return SPID_OK;
 }
 
+int spidgpu_debug_counters(spidgpu_handle h, int64_t* out, int n, int reset) {
+    if (!h || !out || n < 3) return SPID_INVALID_ARGUMENT;
+    cudaSetDevice(h->device);
+    if (sketch_tc_flush_counters(out, reset != 0)) return fail(h, SPID_CUDA_ERROR, "counter readback");
+    return SPID_OK;
+}
+
 const char* spidgpu_last_error(spidgpu_handle h) { return h ? h->last_error.c_str() : ""; }
 
 int64_t spidgpu_launch_count(spidgpu_handle h) { return h ? h->launches : 0; }
@@ -589,10 +590,13 @@ int spidgpu_set_option(spidgpu_handle h, int option, int64_t value) {
     switch (option) {
         case SPIDGPU_OPT_GENERIC_CPQR: h->force_generic_cpqr = value != 0; return SPID_OK;
         case SPIDGPU_OPT_DMMA_SKETCH: h->force_dmma_sketch = value != 0; return SPID_OK;
-        case SPIDGPU_OPT_IMMA_SKETCH: h->force_imma_sketch = value != 0; return SPID_OK;
         case SPIDGPU_OPT_SKETCH_PAIRS:
             if (value < 0 || value > 2) return SPID_INVALID_ARGUMENT;
             h->sketch_pairs = static_cast<int>(value);
+            return SPID_OK;
+        case SPIDGPU_OPT_SKETCH_SEG_ROWS:
+            if (value < 0 || value % 512 || value > 65536) return SPID_INVALID_ARGUMENT;
+            h->sketch_seg_rows = value;
             return SPID_OK;
         case SPIDGPU_OPT_SKETCH_SMS:
             if (value < 0) return SPID_INVALID_ARGUMENT;

@@ -51,23 +51,38 @@ bool cpqr_reg_supported(int64_t rows, int64_t n, int64_t step_cap);
 cudaError_t launch_cpqr_reg(const CpqrParams& p, cudaStream_t stream);
 
 // ---- sketch Y = Omega * A (sketch.cu) -------------------------------------
+// Work decomposition shared by both sketch kernels. A subdomain's column tile
+// is cut into SEGMENTS of kSketchSegRows rows at fixed absolute row offsets
+// (they depend on m only). A work unit is one (subdomain, column tile,
+// segment); each persistent CTA (or CTA pair) takes a contiguous range of
+// whole units, accumulates every segment on its own and writes it to the
+// segment's own partial slot; the reduction sums a tile's slots in segment
+// order. So Y_s is bitwise the same whatever the batch, the grouping, the
+// grid size (SM cap) or the GPU count -- the reference's "bitwise identical
+// regardless of scheduling" contract (
+// proj/tests/test_pipeline.cpp:104-125).
+constexpr int64_t kSketchSegRows = 4096;
 struct SketchPlan {
     int ell_pad;     // Omega rows computed (8..80)
     int mt;          // M tiles of 8 rows (ell_pad = 8*mt)
     int nw;          // N tiles of 8 columns per warp
     int nt;          // columns per CTA tile
     int64_t ntiles_col;   // column tiles per subdomain
-    int64_t nchunk;       // row chunks per subdomain
-    int kc_rows;          // rows per chunk (16 DMMA, 32 or 64 integer-sliced)
-    int64_t total_chunks; // batch * ntiles_col * nchunk
-    int grid;             // CTAs (persistent, balanced contiguous ranges)
-    int max_segs;         // partial slots per CTA
-    int halves = 1;       // partial tiles per slot (2: the integer sketch's slice halves)
-    int pair = 0;         // 1: CTAs run as clusters of two over column-tile pairs (sketch_tc.cu);
-                          // total_chunks then counts pair units and grid stays the CTA count
+    int64_t nchunk;       // row chunks (stages) per subdomain
+    int kc_rows;          // rows per chunk (16 DMMA, 32 integer-sliced)
+    int64_t seg_len;      // chunks per segment (kSketchSegRows / kc_rows)
+    int64_t nseg;         // segments per column tile
+    int64_t total_units;  // batch * (ntiles_col / (1 + pair)) * nseg
+    int grid;             // CTAs (persistent, contiguous ranges of whole units)
+    int halves = 1;       // partial tiles per slot (2: slice halves of a split CTA pair)
+    int pair = 0;         // 1: CTAs run as clusters of two over column-tile pairs (sketch_tc.cu)
     size_t smem;
-    size_t partial_elems; // doubles of the partial workspace
+    size_t partial_elems; // doubles of the partial workspace: batch*ntiles_col*nseg*halves*ell_pad*nt
 };
+// first chunk (in the flat (subdomain, column tile, chunk) order) of unit u
+__host__ __device__ inline int64_t sketch_unit_chunk(int64_t u, int64_t nseg, int64_t seg_len, int64_t nchunk) {
+    return (u / nseg) * nchunk + (u % nseg) * seg_len;
+}
 struct SketchParams {
     const double* A;
     int64_t m, n, lda, strideA, batch;
@@ -78,7 +93,7 @@ struct SketchParams {
     int64_t ldo, stride_o;
     uint64_t seed;
     int64_t sub_base;
-    double* partial;      // [grid][max_segs][ell_pad][nt]
+    double* partial;      // [subdomain][column tile][segment][half][ell_pad][nt]
     double* Y;            // final: Y_s(r, j) at Y + s*strideY + j*ldy + (row0 + r)
     int64_t ldy, strideY;
 };
@@ -86,18 +101,14 @@ bool sketch_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int num_
                       SketchPlan* plan);
 cudaError_t launch_sketch(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap,
                           cudaStream_t stream);
-// fixed-order split-K reduction of the partials into Y (both sketch kernels)
+// fixed-order reduction of the segment partials into Y (both sketch kernels)
 cudaError_t launch_sketch_reduce(const SketchParams& p, const SketchPlan& plan, cudaStream_t stream);
-// exact integer-sliced sketch for the Philox Omega (sketch_i8.cu)
-constexpr int64_t kSketchI8MaxEll = 48;  // Omega rows per launch; wider sketches are sliced
-bool sketch_i8_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int num_sms,
-                         SketchPlan* plan);
-cudaError_t launch_sketch_i8(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap,
-                             cudaStream_t stream);
-// the same on tcgen05.mma kind::i8 with TMEM accumulators (sketch_tc.cu)
+// the exact integer-sliced sketch on tcgen05.mma kind::i8 with TMEM accumulators (sketch_tc.cu)
 constexpr int64_t kSketchTcMaxEll = 64;
+// seg_rows: rows per segment (0 = kSketchSegRows; a multiple of 512, <= 65536)
 bool sketch_tc_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int num_sms, int pair_mode,
-                         SketchPlan* plan);
+                         int64_t seg_rows, SketchPlan* plan);
+int sketch_tc_flush_counters(int64_t* out, bool reset);
 cudaError_t launch_sketch_tc(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap,
                              cudaStream_t stream);
 cudaError_t launch_philox_omega(uint64_t seed, int64_t s, int64_t ell, int64_t m, double* out,
@@ -128,10 +139,10 @@ struct VerifyParams {
     double* ref2;
 };
 int64_t verify_row_blocks(int64_t m);
-struct VerifyPlan {
+struct VerifyPlan {  // same segment units as the sketch (SketchPlan)
     int nwv, ks, nt;
-    int64_t ntiles_col, nchunk, total_chunks;
-    int grid, max_segs;
+    int64_t ntiles_col, nchunk, seg_len, nseg, total_units;
+    int grid;
     size_t part_elems;
 };
 bool verify_make_plan(int64_t m, int64_t n, int64_t batch, int64_t kcap, int num_sms,

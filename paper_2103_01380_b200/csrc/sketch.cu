@@ -13,9 +13,9 @@
 //
 // Design (B200):
 //  * persistent grid, one CTA per SM; the flat (subdomain, column tile,
-//    16-row chunk) space is split into equal contiguous ranges, one per CTA
-//    (stream-K style): perfect balance, and a CTA writes one partial per
-//    tile it touches (<= 2-3), so split-K traffic is ~0.05% of A;
+//    4096-row segment) unit space (kernels.h) is split into contiguous
+//    ranges of whole units, one per CTA; a CTA writes one partial per
+//    segment into that segment's own slot (about 1% of A's bytes);
 //  * A chunks (16 rows x NT columns, 128 B rows) are staged by TMA with
 //    128B swizzle through an S-stage ring; "full" mbarriers carry the TMA
 //    transaction bytes, "empty" mbarriers collect one arrive per warp, so
@@ -32,8 +32,9 @@
 //    each A fragment pair is one 16-byte shared load and the two rows of a
 //    quarter-warp hit opposite 16B-chunk parities under the swizzle: every
 //    fragment load is bank-conflict free;
-//  * partials are reduced by a small second kernel in a fixed order, so Y is
-//    bitwise reproducible run to run (proj/tests/test_matrix_core.cpp:145-153).
+//  * partials are reduced by a small second kernel in segment order, so Y is
+//    bitwise reproducible run to run (proj/tests/test_matrix_core.cpp:145-153)
+//    and independent of the batch, grid and grouping.
 #include <math.h>
 
 #include "common.cuh"
@@ -82,7 +83,7 @@ __device__ __forceinline__ ChunkPos chunk_pos(int64_t g, int64_t nchunk, int64_t
 template <int WM, int MTW, int NW, int OMODE>
 __global__ void __launch_bounds__(kThreads, 1)
     sketch_kernel(const __grid_constant__ CUtensorMap tmap, SketchParams p, int64_t nchunk,
-                  int64_t ntiles_col, int64_t total_chunks, int max_segs) {
+                  int64_t ntiles_col, int64_t nseg, int64_t seg_len, int64_t total_units) {
     using Cfg = SketchCfg<WM, MTW, NW>;
     constexpr int S = Cfg::kStages;
     extern __shared__ unsigned char smem_raw[];
@@ -98,7 +99,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t G = gridDim.x, c = blockIdx.x;
-    const int64_t lo = (c * total_chunks) / G, hi = ((c + 1) * total_chunks) / G;
+    const int64_t lo = sketch_unit_chunk((c * total_units) / G, nseg, seg_len, nchunk);
+    const int64_t hi = sketch_unit_chunk(((c + 1) * total_units) / G, nseg, seg_len, nchunk);
     const int64_t niter = hi - lo;
     if (niter <= 0) return;
 
@@ -182,10 +184,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < NW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    int seg = 0;
     int slot = 0;
     uint32_t par = 0;
-    int64_t kc = lo % nchunk;  // chunk index inside the current tile
+    ChunkPos cq = chunk_pos(lo, nchunk, ntiles_col);  // the chunk being contracted
     for (int64_t it = 0; it < niter; ++it) {
         mbar_wait(&full_a[slot], par);
         mbar_wait(&full_o[slot], par);
@@ -216,10 +217,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             slot = 0;
             par ^= 1u;
         }
-        if (++kc == nchunk || it + 1 == niter) {  // tile boundary: flush partial
-            kc = 0;
-            double* part = p.partial + (static_cast<size_t>(c) * max_segs + seg) *
-                                           (static_cast<size_t>(Cfg::kEllPad) * Cfg::kNt);
+        // last chunk of a segment (ranges end on segment ends): its partial
+        // goes to the segment's own slot
+        if (cq.kc + 1 == nchunk || (cq.kc + 1) % seg_len == 0) {
+            const int64_t unit = (cq.s * ntiles_col + cq.ct) * nseg + cq.kc / seg_len;
+            double* part = p.partial + static_cast<size_t>(unit) * (static_cast<size_t>(Cfg::kEllPad) * Cfg::kNt);
 #pragma unroll
             for (int mt = 0; mt < MTW; ++mt)
 #pragma unroll
@@ -229,63 +231,41 @@ __global__ void __launch_bounds__(kThreads, 1)
                         make_double2(acc[mt][nt][0], acc[mt][nt][1]);
                     acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
                 }
-            ++seg;
+        }
+        if (++cq.kc == nchunk) {
+            cq.kc = 0;
+            if (++cq.ct == ntiles_col) {
+                cq.ct = 0;
+                ++cq.s;
+            }
         }
     }
 }
 
-// Fixed-order reduction of the per-CTA partials of one (subdomain, column
-// tile) into Y (column-major ell x n). Contributors are the CTAs whose chunk
-// range intersects the tile, summed in CTA order. One block per (tile, 8-row
-// slab): partial rows are read coalesced (column fastest) into a padded
-// shared slab, then written out column-major (row fastest).
+// Fixed-order reduction of the segment partials of one (subdomain, column
+// tile) into Y (column-major ell x n): slots summed in segment order (then
+// half order), whichever CTA wrote them. One block per (tile, 8-row slab):
+// partial rows are read coalesced (column fastest) into a padded shared
+// slab, then written out column-major (row fastest).
 constexpr int kRedRows = 8;
 constexpr int kRedMaxNt = 256;
 
-// pair = 1 (sketch_tc.cu CTA pairs): the stream-K units are (subdomain,
-// column-tile pair, stage) over G/2 pairs, and column tile ct was sketched by
-// CTA 2 * pair + ct % 2.
-__global__ void __launch_bounds__(256) sketch_reduce_kernel(SketchParams p, int ell_pad, int nt, int64_t nchunk,
-                                     int64_t ntiles_col, int64_t total_chunks, int G,
-                                     int max_segs, int halves, int pair) {
+__global__ void __launch_bounds__(256) sketch_reduce_kernel(SketchParams p, int ell_pad, int nt, int64_t ntiles_col,
+                                                            int64_t nseg, int halves) {
     __shared__ double slab[kRedRows][kRedMaxNt + 1];
-    __shared__ int cfirst, clast;
     const int nslab = (static_cast<int>(p.ell) + kRedRows - 1) / kRedRows;
     const int64_t tile = blockIdx.x / nslab;
     const int r0 = (blockIdx.x % nslab) * kRedRows;
     const int64_t s = tile / ntiles_col, ct = tile % ntiles_col;
-    const int P = pair ? 2 : 1;
-    const int64_t utile = s * (ntiles_col / P) + ct / P;  // the work-unit tile
-    const int rk = static_cast<int>(ct % P);
-    const int Gu = G / P;
-    const int64_t t0 = utile * nchunk, t1 = t0 + nchunk;
-    if (threadIdx.x == 0) {
-        int64_t cf = (t0 * Gu) / total_chunks;
-        while (cf > 0 && (cf * total_chunks) / Gu > t0) --cf;
-        while (((cf + 1) * total_chunks) / Gu <= t0) ++cf;
-        int64_t cl = cf;
-        while (cl + 1 < Gu && ((cl + 1) * total_chunks) / Gu < t1) ++cl;
-        cfirst = static_cast<int>(cf);
-        clast = static_cast<int>(cl);
-    }
-    __syncthreads();
     const int ncols = static_cast<int>(p.n - ct * nt < nt ? p.n - ct * nt : nt);
     const int nrows = static_cast<int>(p.ell - r0 < kRedRows ? p.ell - r0 : kRedRows);
+    const size_t slot_elems = static_cast<size_t>(ell_pad) * nt;
+    const double* tpart = p.partial + static_cast<size_t>(tile) * nseg * halves * slot_elems;
     for (int e = threadIdx.x; e < nrows * ncols; e += blockDim.x) {
         const int rl = e / ncols, col = e % ncols;  // column fastest: coalesced partial reads
+        const double* src = tpart + (r0 + rl) * nt + col;
         double sum = 0.0;
-        for (int cc = cfirst; cc <= clast; ++cc) {
-            const int64_t lo = (static_cast<int64_t>(cc) * total_chunks) / Gu;
-            const int64_t hi = (static_cast<int64_t>(cc + 1) * total_chunks) / Gu;
-            if (hi <= lo) continue;
-            const int segi = static_cast<int>(utile - lo / nchunk);
-            const size_t cta = static_cast<size_t>(cc) * P + rk;
-            for (int hv = 0; hv < halves; ++hv) {
-                const double* part = p.partial + ((cta * max_segs + segi) * halves + hv) *
-                                                     (static_cast<size_t>(ell_pad) * nt);
-                sum += part[(r0 + rl) * nt + col];
-            }
-        }
+        for (int64_t g = 0; g < nseg * halves; ++g) sum += src[g * slot_elems];
         slab[rl][col] = sum;
     }
     __syncthreads();
@@ -319,8 +299,8 @@ cudaError_t launch_t(const SketchParams& p, const SketchPlan& plan, const CUtens
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(Cfg::kSmem));
     if (e != cudaSuccess) return e;
-    kern<<<plan.grid, kThreads, Cfg::kSmem, stream>>>(*tmap, p, plan.nchunk, plan.ntiles_col,
-                                                      plan.total_chunks, plan.max_segs);
+    kern<<<plan.grid, kThreads, Cfg::kSmem, stream>>>(*tmap, p, plan.nchunk, plan.ntiles_col, plan.nseg,
+                                                      plan.seg_len, plan.total_units);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     static_assert(Cfg::kNt <= kRedMaxNt, "reduce slab too narrow");
@@ -405,17 +385,17 @@ bool sketch_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int num_
     plan->ntiles_col = (n + plan->nt - 1) / plan->nt;
     plan->kc_rows = kKc;
     plan->nchunk = (m + kKc - 1) / kKc;
-    plan->total_chunks = batch * plan->ntiles_col * plan->nchunk;
+    plan->seg_len = kSketchSegRows / kKc;
+    plan->nseg = (plan->nchunk + plan->seg_len - 1) / plan->seg_len;
+    plan->total_units = batch * plan->ntiles_col * plan->nseg;
     int64_t grid = num_sms;
-    if (grid > plan->total_chunks) grid = plan->total_chunks;
+    if (grid > plan->total_units) grid = plan->total_units;
     plan->grid = static_cast<int>(grid);
-    const int64_t per = (plan->total_chunks + grid - 1) / grid;
-    plan->max_segs = static_cast<int>(per / plan->nchunk + 2);
     const int sbytes = (plan->nt + ell_pad) * kKc * 8;
     int stages = kStageBudget / sbytes;
     if (stages > 8) stages = 8;
     plan->smem = 1024 + static_cast<size_t>(stages) * sbytes + 24 * stages;
-    plan->partial_elems = static_cast<size_t>(grid) * plan->max_segs * ell_pad * plan->nt;
+    plan->partial_elems = static_cast<size_t>(batch) * plan->ntiles_col * plan->nseg * ell_pad * plan->nt;
     return true;
 }
 
@@ -423,8 +403,7 @@ cudaError_t launch_sketch_reduce(const SketchParams& p, const SketchPlan& plan, 
     if (plan.nt > kRedMaxNt) return cudaErrorInvalidValue;
     const int nslab = static_cast<int>((p.ell + kRedRows - 1) / kRedRows);
     sketch_reduce_kernel<<<static_cast<unsigned>(p.batch * plan.ntiles_col * nslab), 256, 0, stream>>>(
-        p, plan.ell_pad, plan.nt, plan.nchunk, plan.ntiles_col, plan.total_chunks, plan.grid,
-        plan.max_segs, plan.halves, plan.pair);
+        p, plan.ell_pad, plan.nt, plan.ntiles_col, plan.nseg, plan.halves);
     return cudaGetLastError();
 }
 

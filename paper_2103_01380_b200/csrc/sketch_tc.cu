@@ -2,8 +2,8 @@
 // integer-sliced contraction on the 5th-generation tensor cores
 // (tcgen05.mma kind::i8, accumulators in TMEM).
 //
-// Same reference role as sketch_i8.cu (the north star's Gaussian
-// sketch in place of subsample/subsample_column, proj/src/grid.cpp:136-150;
+// The north star's Gaussian sketch in place of subsample/subsample_column
+// (proj/src/grid.cpp:136-150;
 // CPU restatement matmul(Omega, A), proj/src/dense_matrix.cpp:38-53): the
 // Philox Omega is integer-valued (Omega = Q/32, |Q| <= 117, philox.cuh), each
 // column of A is a fixed-point integer v = rint(x 2^(50-E)) per period (E =
@@ -11,18 +11,19 @@
 // DFMA as the mantissa of x 2^(50-E) + 1.5 2^52: its low 56 bits are the
 // offset-binary u = v + 7 2^51, split into 7 unsigned byte slices, each
 // contracted exactly with Q in int32; an 8th MMA against an all-ones tile
-// accumulates sum_k Q, and the offset is removed exactly (int64) at flush. sketch_i8.cu does this with register-fed IMMA.16832, whose issue
-// rate (8 cycles per m16n8k32 per SMSP) bounds it at ~76% of HBM; here the
-// contraction runs on UTCIMMA at 4x the rate, so the kernel is bound by the
-// HBM stream of A.
+// accumulates sum_k Q, and the offset is removed exactly (int64) at flush.
+// A register-fed IMMA.16832 version of the same contraction (round 1, now
+// retired) was bound by its issue rate (8 cycles per m16n8k32 per SMSP) at
+// ~76% of HBM; on UTCIMMA the kernel is bound by the HBM stream of A.
 //
 // Formulation: Y_s^T (n x ell) = A_s^T (n x m) * Omega_s^T (m x ell), per CTA
 // tile of 128 snapshots: D_t (M=128 snapshots x N=ell_pad, int32, TMEM
 // columns [N t, N t + N)) += slice_t(A^T) (128 x 32, K-major) *
 // Q^T (32 x N, K-major), one MMA per slice per 32-row stage.
 //
-// Warp roles (512 threads, persistent, one CTA per SM, stream-K over
-// (subdomain, 128-column tile, 32-row stage) like sketch.cu):
+// Warp roles (512 threads, persistent, one CTA per SM, contiguous ranges of
+// whole (subdomain, 128-column tile, 4096-row segment) units like sketch.cu,
+// kernels.h):
 //   warps 0-7   (80 registers) Omega: warps 0, 2..7 run Philox + quantile
 //               table -> K-major int8 tile, at most one task per lane per
 //               stage; warp 0's lane 0 also keeps the A ring full (two
@@ -36,8 +37,19 @@
 //               K-major slice tile. A warp owns its 16 D rows: its rare
 //               flushes read them (tcgen05.ld 16x64b) into the fp64 partial
 //               and zero them (tcgen05.st), without involving another warp.
-// A warp flushes its rows at segment ends, every 2048 stages (|D| < 2^31)
-// and when one of its columns exceeds its exponent headroom.
+// A warp flushes its rows at segment ends (128 stages, so |D| < 2^31), when
+// one of its columns exceeds its exponent headroom, and when a column's
+// magnitude falls more than kFallback binades below its epoch's (so a
+// spike cannot coarsen the rest of the segment).
+//
+// Accuracy contract (tests/test_gpu_sketch_i8.py). Each entry x of an epoch
+// with exponent E is rounded once, to a multiple of 2^(E-50), and everything
+// after that is exact integer arithmetic, so per column j
+//   |Y(i,j) - (Omega A)(i,j)| <= sum_k |Omega(i,k)| 2^(E_k - 51) + fp64 rounding of the flush sums,
+// E_k the exponent of the epoch holding row k: 2^(E_k-51) <= 2^-47 of the
+// epoch's first-stage maximum, and (fallback) at most 2^(kFallback-47) of
+// the row's own 32-row stage maximum. Epochs start at absolute segment
+// starts, so the result does not depend on how subdomains are batched.
 #include <math.h>
 
 #include <type_traits>
@@ -69,12 +81,17 @@ constexpr int kHeadroom = 3;
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
 constexpr int kOffsetHi = 7 << 19;             // kOffset = 7 * 2^51 = kOffsetHi * 2^32
 constexpr int kEbMin = 9;
-constexpr int kPeriodStages = 2048;   // 65536 rows: 65536 * 117 * 255 < 2^31
+constexpr int kFallback = 24;         // restart an epoch when a stage's max is 2^24 below its scale
+static_assert(kSketchSegRows / kRows <= 2048, "a segment's int32 sums stay exact: 65536 * 117 * 255 < 2^31");
 constexpr int kBoxBytes = 16 * kM * 8;              // 16 rows x 128 columns fp64
 constexpr int kAStageBytes = 2 * kBoxBytes;         // 32 KB
 constexpr int kAStages = 5;
 constexpr int kSliceBytes = kM * kRows;             // 4 KB per slice tile
 constexpr int kBStages = 2;
+
+// instrumentation (spidgpu_debug_counters): converter-warp flushes by cause
+// [segment end, headroom overflow, magnitude fallback]; atomics only on flushes
+__device__ unsigned long long g_tc_flushes[3];
 
 template <int NPAD>
 struct TcCfg {
@@ -224,6 +241,51 @@ __device__ __forceinline__ double2 unfix_scale(int eb) {
                         __longlong_as_double(static_cast<long long>(e - e1 + 1023) << 52));
 }
 
+// A converter warp's flush of its 16 TMEM lanes (all 8 accumulators): the
+// exact integer sums -> fp64 partial of the segment (scaled by the epoch's
+// exponent ebf; poisoned columns become NaN at the segment's final flush);
+// `zero` clears the lanes for an epoch restart inside the segment. Kept out
+// of line: flushes are rare (segment ends, exponent restarts), and inlining
+// their 8 x 8 TMEM loads into the converter loop raised its register
+// pressure enough for the compiler to rematerialise addresses every stage.
+template <int NPAD>
+__device__ __noinline__ void tc_flush_rows(uint32_t taddr, double* part, int ebf, int psf, int pf, int col_f,
+                                           bool final_flush, bool zero, bool first) {
+    const double2 u = unfix_scale(ebf);
+#pragma unroll 1
+    for (int g0 = 0; g0 < NPAD; g0 += 16) {
+        // exact: sum_t 2^(8t) D_t - kOffset * D_7 as hi * 2^32 + lo, for
+        // columns g0 + pf + 2j of this thread's D row
+        uint32_t v[kSlices + 1][8];
+#pragma unroll
+        for (int t = 0; t <= kSlices; ++t) tmem_ld16x64b_x8(taddr + NPAD * t + g0, v[t]);
+        tmem_ld_wait();
+        if (zero) {
+#pragma unroll
+            for (int t = 0; t <= kSlices; ++t) tmem_st16x64b_x8_zero(taddr + NPAD * t + g0);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            long long lo64 = 0, hi64 = 0;
+#pragma unroll
+            for (int t = 0; t <= kSlices; ++t) {
+                const long long d = static_cast<int>(v[t][j]);
+                if (t < 4)
+                    lo64 += d * (1LL << (8 * t));
+                else if (t < kSlices)
+                    hi64 += d * (1LL << (8 * (t - 4)));
+                else
+                    hi64 -= d * kOffsetHi;
+            }
+            double val = fma(static_cast<double>(hi64), 4294967296.0, static_cast<double>(lo64)) * u.x * u.y;
+            if (final_flush && psf) val = __longlong_as_double(0x7ff8000000000000LL);
+            double* dst = part + static_cast<size_t>(g0 + pf + 2 * j) * kM + col_f;
+            *dst = first ? val : *dst + val;
+        }
+    }
+    if (zero) tmem_st_wait();
+}
+
 // kPair: the CTAs run as clusters of two that sketch the two column tiles
 // (128 snapshots each) of the same subdomain over the same 32-row stages, so
 // each generates HALF of every stage's Omega tile and writes it into both
@@ -236,7 +298,7 @@ __device__ __forceinline__ double2 unfix_scale(int eb) {
 template <int NPAD, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchParams p, int64_t nchunk,
-                     int64_t ntiles_col, int64_t total_chunks, int max_segs) {
+                     int64_t ntiles_col, int64_t nseg, int64_t seg_len, int64_t total_units) {
     constexpr int P = kPair ? 2 : 1;
     using Cfg = TcCfg<NPAD>;
     extern __shared__ unsigned char smem_raw[];
@@ -258,7 +320,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t c = blockIdx.x;
     const uint32_t rank = kPair ? cluster_ctarank() : 0u;
     const int64_t G = gridDim.x / P, cu = c / P;  // work-unit owners: CTAs, or CTA pairs
-    const int64_t lo = (cu * total_chunks) / G, hi = ((cu + 1) * total_chunks) / G;
+    const int64_t lo = sketch_unit_chunk((cu * total_units) / G, nseg, seg_len, nchunk);
+    const int64_t hi = sketch_unit_chunk(((cu + 1) * total_units) / G, nseg, seg_len, nchunk);
     const int niter = static_cast<int>(hi - lo);
     if (niter <= 0) return;  // both CTAs of a pair share the range
 
@@ -313,11 +376,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
         constexpr uint32_t kIdU = idesc_i8(NPAD, false);
         const uint64_t ones_desc = smem_desc(ones_s, 0, 0);
-        auto issue_mma = [&](int it) {
+        auto issue_mma = [&](int it, int seg_pos) {
             const int sl = it % kBStages;
             mbar_wait(&b_full[sl], (it / kBStages) & 1);
             tc_fence_after();
-            const uint32_t acc = it > 0 ? 1u : 0u;  // flushed TMEM rows are zeroed by their owners
+            // a segment's first stage overwrites D (its owners read the old
+            // segment out before arriving); epoch restarts inside a segment
+            // zero their rows themselves
+            const uint32_t acc = seg_pos != 0 ? 1u : 0u;
             const uint32_t st = b_s + sl * Cfg::kBStageBytes;
             const uint64_t bdesc = smem_desc(st + kSlices * kSliceBytes, NPAD * 16, 128);
 #pragma unroll
@@ -345,8 +411,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (warp == 0 && lane == 0)
             for (int it = 0; it < kAStages && it < niter; ++it) issue_tma(it);
         if (warp == 1) {  // dedicated MMA issuer: no Omega work, so MMAs go out as soon as a stage is full
-            if (lane == 0)
-                for (int it = 0; it < niter; ++it) issue_mma(it);
+            if (lane == 0) {
+                // position inside the current segment (ranges start on segment starts)
+                int sp = 0, kc = cp.kc;
+                const int nch = static_cast<int>(nchunk), sl = static_cast<int>(seg_len);
+                for (int it = 0; it < niter; ++it) {
+                    issue_mma(it, sp);
+                    if (++kc == nch) kc = sp = 0;
+                    else if (++sp == sl) sp = 0;
+                }
+            }
         } else
         for (int it = 0; it < niter; ++it) {
             const int sl = it % kBStages;
@@ -417,6 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // Flush: tcgen05.ld/st .16x64b touch only the warp's 16 lanes (lane L
         // = 8 (t & 1) + (t >> 2), column parity (t >> 1) & 1 per thread t), so
         // a column's overflow handling and flushes never involve another warp.
+        ChunkPos cp = chunk_pos(lo, nchunk, ntiles_col);
         const int q = warp & 3, hh = (warp - 8) >> 2;
         const int cc = lane & 15, b = lane >> 4;
         const int col = q * 32 + hh * 16 + cc;
@@ -424,62 +499,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int lf = 8 * (lane & 1) + (lane >> 2), pf = (lane >> 1) & 1;  // flush: D lane, column parity
         const int col_f = q * 32 + hh * 16 + lf;
         int eb = kEbMin, poison = 0;
-        uint32_t thr = 0;
+        uint32_t thr = 0, thr_lo = 0;
         double sclx = 0.0, scly = 1.0;
         bool tiny = false;
-        int seg = 0;
-        bool first = true, pending = false;  // pending: this warp's D rows hold unflushed stages
-        int psteps = 0;
-        ChunkPos cp = chunk_pos(lo, nchunk, ntiles_col);
+        bool pending = false;  // this warp's D rows hold unflushed stages
+        // partial slot of the current segment (absolute: (tile, segment));
+        // pre-decremented so the first segment start lands on it
+        int seg_slot = static_cast<int>((static_cast<int64_t>(cp.s) * ntiles_col * P + cp.ct * P + rank) * nseg +
+                                        cp.kc / seg_len) - 1;
+        bool seg_first = true; // its first flush stores, later ones add
+        int seg_left = 0;      // stages left in the current segment (ranges start on segment starts)
         const int nch = static_cast<int>(nchunk), ntc = static_cast<int>(ntiles_col);
 
-        // D rows of this warp (all columns of all 8 accumulators) -> fp64
-        // partial of segment `seg` with each row's exponent; optionally zero
-        // them for the next accumulation period
+        // the current epoch's D rows (this warp's 16 TMEM lanes, all 8
+        // accumulators) -> fp64 partial of its segment, scaled by the epoch's
+        // exponent; `zero` clears them for an epoch restart inside the
+        // segment (at a segment start the next MMA overwrites them instead)
         auto flush = [&](int it_last, bool final_flush, bool zero) {
             mbar_wait(&b_empty[it_last % kBStages], (it_last / kBStages) & 1);  // MMAs <= it_last done
             tc_fence_after();
-            double* part = p.partial + (static_cast<size_t>(c) * max_segs + seg) *
-                                           (static_cast<size_t>(NPAD) * kM);
-            const int ebf = __shfl_sync(0xffffffffu, eb, lf);       // lane lf converts column lf (b = 0)
-            const int psf = __shfl_sync(0xffffffffu, poison, lf);
-            const double2 u = unfix_scale(ebf);
-#pragma unroll 1
-            for (int g0 = 0; g0 < NPAD; g0 += 16) {
-                // exact: sum_t 2^(8t) D_t - kOffset * D_7 as hi * 2^32 + lo, for
-                // columns g0 + pf + 2j of D row lf
-                long long lo64[8], hi64[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) lo64[j] = hi64[j] = 0;
-#pragma unroll
-                for (int t = 0; t <= kSlices; ++t) {
-                    uint32_t v[8];
-                    tmem_ld16x64b_x8(tmem + lane_base + NPAD * t + g0, v);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const long long d = static_cast<int>(v[j]);
-                        if (t < 4)
-                            lo64[j] += d * (1LL << (8 * t));
-                        else if (t < kSlices)
-                            hi64[j] += d * (1LL << (8 * (t - 4)));
-                        else
-                            hi64[j] -= d * kOffsetHi;
-                    }
-                    if (zero) tmem_st16x64b_x8_zero(tmem + lane_base + NPAD * t + g0);
-                }
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    double val = fma(static_cast<double>(hi64[j]), 4294967296.0, static_cast<double>(lo64[j])) *
-                                 u.x * u.y;
-                    if (final_flush && psf) val = __longlong_as_double(0x7ff8000000000000LL);
-                    double* dst = part + static_cast<size_t>(g0 + pf + 2 * j) * kM + col_f;
-                    *dst = first ? val : *dst + val;
-                }
-            }
-            if (zero) tmem_st_wait();
+            tc_flush_rows<NPAD>(tmem + lane_base, p.partial + static_cast<int64_t>(seg_slot) * (NPAD * kM),
+                                __shfl_sync(0xffffffffu, eb, lf),  // lane lf converts column lf (b = 0)
+                                __shfl_sync(0xffffffffu, poison, lf), pf, col_f, final_flush, zero, seg_first);
             tc_fence_before();
-            first = false;
         };
 
         // rows [16 b, 16 b + 16) of column col of stage it: 8 conflict-free 16B loads
@@ -508,30 +550,38 @@ __global__ void __launch_bounds__(kThreads, 1)
 
         auto step = [&](int it, const double (&xc)[16], uint32_t mx, double (&xn)[16]) -> uint32_t {
             const int sb = it % kBStages;
-            const bool new_seg = it == 0 || cp.kc == 0;
-            const bool fresh = new_seg || psteps >= kPeriodStages;
-            if (__any_sync(0xffffffffu, fresh || mx >= thr)) {  // warp-uniform, rare
+            const bool new_seg = seg_left == 0;
+            if (__any_sync(0xffffffffu, new_seg || mx >= thr || mx < thr_lo)) {  // warp-uniform, rare
+                const bool over = __any_sync(0xffffffffu, mx >= thr);
                 if (pending) {
                     // a new segment closes the old one (final: poison -> NaN);
-                    // otherwise the rows restart a period or an exponent epoch.
-                    // Either way the rows are zeroed: the MMAs always accumulate.
-                    flush(it - 1, cp.kc == 0, true);
-                    if (cp.kc == 0) {
-                        ++seg;
-                        first = true;
-                    }
+                    // otherwise the rows restart an exponent epoch in the
+                    // segment and are zeroed (the MMAs keep accumulating)
+                    if (lane == 0) atomicAdd(&g_tc_flushes[new_seg ? 0 : over ? 1 : 2], 1ull);
+                    flush(it - 1, new_seg, !new_seg);
                 }
-                if (new_seg) poison = 0;
+                if (new_seg) {
+                    // tiles follow each other in the flat order, each nseg slots
+                    // wide; a pair's CTAs skip their peer's tile
+                    seg_slot += (cp.kc == 0 && pending) ? 1 + (P - 1) * static_cast<int>(nseg) : 1;
+                    seg_first = true;
+                    poison = 0;
+                    seg_left = min(static_cast<int>(seg_len), nch - cp.kc);
+                } else if (pending) {
+                    seg_first = false;
+                }
                 if (mx >= 0x7ff00000u) poison = 1;
                 eb = column_eb(mx);
                 // |x| < 2^(E+1) keeps |v| < 2^51: u = v + kOffset stays a 7-byte integer
                 thr = poison ? 0xffffffffu : (eb >= 2046 ? 0x7ff00000u : static_cast<uint32_t>(eb + 1) << 20);
+                const int elo = eb - 1 - kHeadroom - kFallback;
+                thr_lo = poison || elo <= 0 ? 0u : static_cast<uint32_t>(elo) << 20;
                 const double2 sc2 = fix_scale(eb);
                 sclx = sc2.x;
                 scly = sc2.y;
                 tiny = __any_sync(0xffffffffu, scly != 1.0);
-                psteps = 0;
             }
+            --seg_left;
             const bool more = it + 1 < niter;
             if (more) load(it + 1, xn);
             // one DFMA per entry -- t = RN(x 2^(P-E) + 1.5 2^52), whose low 56
@@ -584,7 +634,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&b_full[sb]);
             pending = true;
-            ++psteps;
             advance(cp, nch, ntc);
             return more ? col_max(it + 1, xn) : 0u;
         };
@@ -596,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mx = step(it, xa, mx, xb);
             if (it + 1 < niter) mx = step(it + 1, xb, mx, xa);
         }
-        // final flush of the last segment
+        // final flush: the range ends on a segment end
         flush(niter - 1, true, false);
     }
     if constexpr (kPair)
@@ -630,10 +679,11 @@ cudaError_t launch_t(const SketchParams& p, const SketchPlan& plan, const CUtens
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, kern, *tmap, p, plan.nchunk, ntiles_u, plan.total_chunks, plan.max_segs);
+        e = cudaLaunchKernelEx(&cfg, kern, *tmap, p, plan.nchunk, ntiles_u, plan.nseg, plan.seg_len,
+                               plan.total_units);
     } else {
-        kern<<<plan.grid, kThreads, Cfg::kSmem, stream>>>(*tmap, p, plan.nchunk, ntiles_u, plan.total_chunks,
-                                                          plan.max_segs);
+        kern<<<plan.grid, kThreads, Cfg::kSmem, stream>>>(*tmap, p, plan.nchunk, ntiles_u, plan.nseg, plan.seg_len,
+                                                          plan.total_units);
         e = cudaGetLastError();
     }
     if (e != cudaSuccess) return e;
@@ -682,8 +732,19 @@ int max_pairs_for(int ell_pad) {
 
 }  // namespace
 
+int sketch_tc_flush_counters(int64_t* out, bool reset) {
+    unsigned long long v[3] = {0, 0, 0};
+    if (cudaMemcpyFromSymbol(v, g_tc_flushes, sizeof v) != cudaSuccess) return 1;
+    for (int i = 0; i < 3; ++i) out[i] = static_cast<int64_t>(v[i]);
+    if (reset) {
+        const unsigned long long z[3] = {0, 0, 0};
+        if (cudaMemcpyToSymbol(g_tc_flushes, z, sizeof z) != cudaSuccess) return 1;
+    }
+    return 0;
+}
+
 bool sketch_tc_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int num_sms, int pair_mode,
-                         SketchPlan* plan) {
+                         int64_t seg_rows, SketchPlan* plan) {
     if (m < 1 || n < 1 || batch < 1 || ell < 1 || ell > kSketchTcMaxEll) return false;
     plan->ell_pad = static_cast<int>(16 * ((ell + 15) / 16));
     plan->mt = plan->ell_pad / 16;
@@ -701,14 +762,15 @@ bool sketch_tc_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int n
     const int pairs = want && num_sms >= 2 && plan->ntiles_col % 2 == 0 ? max_pairs_for(plan->ell_pad) : 0;
     plan->pair = pairs > 0 && 2 * pairs >= num_sms - 1 ? 1 : 0;
     const int P = plan->pair ? 2 : 1;
-    plan->total_chunks = batch * (plan->ntiles_col / P) * plan->nchunk;  // work units
+    plan->seg_len = (seg_rows > 0 ? seg_rows : kSketchSegRows) / kRows;
+    plan->nseg = (plan->nchunk + plan->seg_len - 1) / plan->seg_len;
+    plan->total_units = batch * (plan->ntiles_col / P) * plan->nseg;
     int64_t owners = plan->pair ? std::min<int64_t>(pairs, num_sms / 2) : num_sms;
-    if (owners > plan->total_chunks) owners = plan->total_chunks;
+    if (owners > plan->total_units) owners = plan->total_units;
     plan->grid = static_cast<int>(owners * P);
-    const int64_t per = (plan->total_chunks + owners - 1) / owners;
-    plan->max_segs = static_cast<int>(per / plan->nchunk + 2);
     plan->smem = 0;
-    plan->partial_elems = static_cast<size_t>(plan->grid) * plan->max_segs * plan->ell_pad * plan->nt;
+    plan->partial_elems =
+        static_cast<size_t>(batch) * plan->ntiles_col * plan->nseg * plan->ell_pad * plan->nt;
     return true;
 }
 

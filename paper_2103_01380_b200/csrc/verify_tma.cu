@@ -9,8 +9,9 @@
 // and HBM at k = 32.
 //
 // Layout of the work (mirrors sketch.cu):
-//  * persistent grid, one CTA per SM, equal contiguous ranges of the flat
-//    (subdomain, column tile, 16-row chunk) space (stream-K);
+//  * persistent grid, one CTA per SM, contiguous ranges of whole
+//    (subdomain, column tile, 4096-row segment) units (as the sketch,
+//    kernels.h), so the sums do not depend on the batch or the grid;
 //  * 1 producer warp issues two TMA boxes per chunk -- A (16 rows x NT
 //    columns) and the skeleton rows (16 rows x 4*KS columns), both 128B
 //    swizzled -- into an S-stage mbarrier ring;
@@ -19,9 +20,9 @@
 //    accumulator row (mt, grow) is chunk row 2*grow + mt, so one 16-byte
 //    shared load yields both M tiles' skeleton fragment, and one yields the
 //    two A values each accumulator pair is compared with (conflict free);
-//  * err/ref are summed per lane, reduced per warp, written per (CTA, tile
-//    segment, warp) and summed in a fixed order by a second kernel, so the
-//    result is bitwise reproducible run to run.
+//  * err/ref are summed per lane, reduced per warp, written per (segment,
+//    warp) and summed in a fixed order by a second kernel, so the result is
+//    bitwise reproducible run to run and for any batching.
 #include <type_traits>
 
 #include "common.cuh"
@@ -49,8 +50,8 @@ struct VCfg {
 template <int NWV, int KS>
 __global__ void __launch_bounds__(kThreadsV, 1)
     verify_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmS,
-                      VerifyParams p, int64_t nchunk, int64_t ntiles_col, int64_t total_chunks,
-                      int max_segs, double* __restrict__ part) {
+                      VerifyParams p, int64_t nchunk, int64_t ntiles_col, int64_t nseg, int64_t seg_len,
+                      int64_t total_units, double* __restrict__ part) {
     using Cfg = VCfg<NWV, KS>;
     constexpr int S = Cfg::kStages;
     extern __shared__ unsigned char smem_raw[];
@@ -64,7 +65,8 @@ __global__ void __launch_bounds__(kThreadsV, 1)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t G = gridDim.x, c = blockIdx.x;
-    const int64_t lo = (c * total_chunks) / G, hi = ((c + 1) * total_chunks) / G;
+    const int64_t lo = sketch_unit_chunk((c * total_units) / G, nseg, seg_len, nchunk);
+    const int64_t hi = sketch_unit_chunk(((c + 1) * total_units) / G, nseg, seg_len, nchunk);
     const int64_t niter = hi - lo;
     if (niter <= 0) return;
     if (tid == 0) {
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(kThreadsV, 1)
     };
     load_tile(tile);
     double err = 0.0, ref = 0.0;
-    int slot = 0, seg = 0;
+    int slot = 0;
     uint32_t par = 0;
     for (int64_t it = 0; it < niter; ++it) {
         mbar_wait(&full[slot], par);
@@ -181,8 +183,7 @@ __global__ void __launch_bounds__(kThreadsV, 1)
             slot = 0;
             par ^= 1u;
         }
-        if (++kc == nchunk || it + 1 == niter) {  // tile end: flush this warp's sums
-            kc = 0;
+        if (kc + 1 == nchunk || (kc + 1) % seg_len == 0) {  // segment end: flush this warp's sums
             double e2 = err, r2 = ref;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) {
@@ -190,42 +191,30 @@ __global__ void __launch_bounds__(kThreadsV, 1)
                 r2 += __shfl_xor_sync(0xffffffffu, r2, off);
             }
             if (lane == 0) {
-                double* dst = part + ((static_cast<size_t>(c) * max_segs + seg) * kCons + warp) * 2;
+                double* dst = part + ((static_cast<size_t>(tile) * nseg + kc / seg_len) * kCons + warp) * 2;
                 dst[0] = e2;
                 dst[1] = r2;
             }
             err = ref = 0.0;
-            ++seg;
+        }
+        if (++kc == nchunk) {
+            kc = 0;
             ++tile;
             if (it + 1 < niter) load_tile(tile);
         }
     }
 }
 
-// err2[s], ref2[s]: fixed-order sum over the subdomain's column tiles, the
-// CTAs whose range touched each tile (CTA order) and their warps.
-__global__ void verify_tma_finish(VerifyParams p, int64_t nchunk, int64_t ntiles_col,
-                                  int64_t total_chunks, int G, int max_segs, const double* part) {
+// err2[s], ref2[s]: fixed-order sum over the subdomain's column tiles,
+// their segments and the warps' partials.
+__global__ void verify_tma_finish(VerifyParams p, int64_t ntiles_col, int64_t nseg, const double* part) {
     const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (s >= p.batch) return;
     double e = 0.0, r = 0.0;
-    for (int64_t ct = 0; ct < ntiles_col; ++ct) {
-        const int64_t tile = s * ntiles_col + ct;
-        const int64_t t0 = tile * nchunk, t1 = t0 + nchunk;
-        int64_t cf = (t0 * G) / total_chunks;
-        while (cf > 0 && (cf * total_chunks) / G > t0) --cf;
-        while (((cf + 1) * total_chunks) / G <= t0) ++cf;
-        for (int64_t cc = cf; cc < G; ++cc) {
-            const int64_t lo = (cc * total_chunks) / G, hi = ((cc + 1) * total_chunks) / G;
-            if (lo >= t1) break;
-            if (hi <= lo) continue;
-            const int64_t segi = tile - lo / nchunk;
-            const double* src = part + (static_cast<size_t>(cc) * max_segs + segi) * kCons * 2;
-            for (int w = 0; w < kCons; ++w) {
-                e += src[2 * w];
-                r += src[2 * w + 1];
-            }
-        }
+    const double* src = part + static_cast<size_t>(s) * ntiles_col * nseg * kCons * 2;
+    for (int64_t g = 0; g < ntiles_col * nseg * kCons; ++g) {
+        e += src[2 * g];
+        r += src[2 * g + 1];
     }
     p.err2[s] = e;
     p.ref2[s] = r;
@@ -239,12 +228,12 @@ cudaError_t launch_t(const VerifyParams& p, const VerifyPlan& plan, const CUtens
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(Cfg::kSmem));
     if (e != cudaSuccess) return e;
-    kern<<<plan.grid, kThreadsV, Cfg::kSmem, stream>>>(*tA, *tS, p, plan.nchunk, plan.ntiles_col,
-                                                       plan.total_chunks, plan.max_segs, part);
+    kern<<<plan.grid, kThreadsV, Cfg::kSmem, stream>>>(*tA, *tS, p, plan.nchunk, plan.ntiles_col, plan.nseg,
+                                                       plan.seg_len, plan.total_units, part);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    verify_tma_finish<<<static_cast<unsigned>((p.batch + 127) / 128), 128, 0, stream>>>(
-        p, plan.nchunk, plan.ntiles_col, plan.total_chunks, plan.grid, plan.max_segs, part);
+    verify_tma_finish<<<static_cast<unsigned>((p.batch + 127) / 128), 128, 0, stream>>>(p, plan.ntiles_col,
+                                                                                         plan.nseg, part);
     return cudaGetLastError();
 }
 
@@ -292,13 +281,13 @@ bool verify_make_plan(int64_t m, int64_t n, int64_t batch, int64_t kcap, int num
     plan->nt = kCons * 8 * nwv;
     plan->ntiles_col = (n + plan->nt - 1) / plan->nt;
     plan->nchunk = (m + kRows - 1) / kRows;
-    plan->total_chunks = batch * plan->ntiles_col * plan->nchunk;
+    plan->seg_len = kSketchSegRows / kRows;
+    plan->nseg = (plan->nchunk + plan->seg_len - 1) / plan->seg_len;
+    plan->total_units = batch * plan->ntiles_col * plan->nseg;
     int64_t grid = num_sms;
-    if (grid > plan->total_chunks) grid = plan->total_chunks;
+    if (grid > plan->total_units) grid = plan->total_units;
     plan->grid = static_cast<int>(grid);
-    const int64_t per = (plan->total_chunks + grid - 1) / grid;
-    plan->max_segs = static_cast<int>(per / plan->nchunk + 2);
-    plan->part_elems = static_cast<size_t>(grid) * plan->max_segs * kCons * 2;
+    plan->part_elems = static_cast<size_t>(plan->total_units) * kCons * 2;
     return true;
 }
 
