@@ -68,11 +68,58 @@ def workload(cfg_name, rank, world):
     if cfg.per_gpu_subdomains:
         field, first, count = weak_range(cfg, rank, world)
     else:  # fixed-size configs: contiguous share of the config's own field
-        from paper_2103_01380_b200.distributed import contiguous_range
-
-        lo, hi = contiguous_range(cfg.subdomains, rank, world)
+        lo, hi = (rank * cfg.subdomains) // world, ((rank + 1) * cfg.subdomains) // world
         field, first, count = cfg, lo, hi - lo
     return cfg, field, first, count
+
+
+FAMILY = {0: "analytic incompressible TGV (u, v, w, p)", 1: "compressible TGV (rho, u, v, w, E)",
+          2: "compressible TGV + 64 seeded Fourier modes (rho, u, v, w, E)"}
+
+
+def describe(cfg, field, first, count, world):
+    """config.workload: the field family, shapes, rank rule and partition."""
+    rule = (f"blocked rank rule (steps of {cfg.kstep} up to {cfg.k}, sketch error <= {cfg.tol})"
+            if cfg.adaptive else f"fixed rank k={cfg.k}")
+    part = ("global blocks dealt round-robin over ranks (heavy = upper half of the block grid, +256 "
+            "high-wavenumber modes)" if cfg.adaptive else
+            f"global blocks [{cfg.per_gpu_subdomains}r, {cfg.per_gpu_subdomains}r+{cfg.per_gpu_subdomains}) on rank r"
+            if cfg.per_gpu_subdomains else f"contiguous block ranges (rank 0: [{first}, {first + count}))")
+    return (f"{cfg.name}: {count} subdomains on rank 0 of {cfg.block}^3 x {cfg.qois} QoIs x {cfg.n} "
+            f"snapshots ({cfg.m}x{cfg.n} fp64), {rule}, p={cfg.p} (ell={cfg.ell}), in-kernel Philox Omega "
+            f"(discretised Gaussian Q/32); {part} of the {field.grid}^3 {FAMILY[field.kind]} field, "
+            f"{world} rank(s)")
+
+
+def _free_port():
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(args):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: start the N ranks
+    ourselves, exactly as the driver's torchrun launch would (one process per
+    GPU, rendezvous on 127.0.0.1); rank 0 prints the line."""
+    import subprocess
+
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def check_world(args):
+    """The rank count must be the GPU count asked for: a mismatch would
+    report N GPUs' worth of work measured on another number of ranks."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}: launch with "
+                                   f"--nproc-per-node {args.gpus} (or run without torchrun and let "
+                                   f"bench.py start the ranks)"}), file=sys.stderr, flush=True)
+        return False
+    return True
 
 
 def _allreduce(t, op=None):
@@ -152,26 +199,38 @@ class ClockSampler:
 
 
 # ---- the reference CPU path (oracle/_ref) ---------------------------------------
-def reference_inputs(cfg, field, first, count, threads, device=0, a_dev=None):
-    """A bounded sample of the workload for the CPU reference: one subdomain
-    per host thread (A_s from the same device generator, untimed) and the
-    exact Philox Omega_s our kernel uses, materialised for the reference's
-    matmul. Inputs only -- the timed path below is the reference's code."""
-    import torch
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
 
-    from paper_2103_01380_b200 import spid
-    from paper_2103_01380_b200.engine import Engine
+    return platform.processor() or "unknown"
+
+
+def reference_inputs(cfg, field, first, count, threads, a_dev=None):
+    """A bounded sample of the workload for the CPU reference: one subdomain
+    per host thread and the exact Philox Omega_s our kernel uses,
+    materialised for the reference's matmul. Inputs only, untimed.
+
+    The reference arm builds both on the CPU (oracle/workload.c, the same
+    field generator and Omega definition -- tests/test_workload_oracle.py),
+    so its process never loads libspidgpu.so. Our own arm's cpu_baseline
+    passes its device-resident A (a_dev) so both sides see the same bits."""
+    import oracle
 
     nsamp = max(1, min(threads, count))
-    eng = None
+    o = oracle.port()
     if a_dev is None:
-        eng = Engine(device)
-        a_dev = eng.generate(field, first, nsamp)
-    a = a_dev[:nsamp].cpu().numpy()  # (S, n, m) == S column-major m x n
-    om = np.stack([np.ascontiguousarray(spid.philox_omega(cfg.seed, first + s, cfg.ell, cfg.m).T)
+        a = o.field_generate(field.field_dict(), first, nsamp, threads=threads)  # (S, n, m)
+    else:
+        a = a_dev[:nsamp].cpu().numpy()
+    om = np.stack([np.ascontiguousarray(o.philox_omega(cfg.seed, first + s, cfg.ell, cfg.m).T)
                    for s in range(nsamp)])  # (S, m, ell) == S column-major ell x m
-    del eng, a_dev
-    torch.cuda.empty_cache()
     return a, om
 
 
@@ -186,7 +245,7 @@ def reference_time(cfg, a, om, threads):
     nsamp = a.shape[0]
     raw = 8.0 * cfg.m * cfg.n * nsamp
     return {"value": raw / secs / 1e9, "unit": "GB/s", "cores": int(threads),
-            "kind": "reference", "seconds": secs,
+            "kind": "reference", "seconds": secs, "cpu_model": cpu_model(),
             "sample": f"{nsamp} of the workload's subdomains ({cfg.m}x{cfg.n} fp64 each, "
                       f"{raw / 1e9:.2f} GB), one per std::thread, Philox Omega materialised "
                       f"for the reference's matmul; compress = matmul + column_id + "
@@ -195,13 +254,39 @@ def reference_time(cfg, a, om, threads):
             "ranks_ok": bool(np.all(ranks == cfg.k))}
 
 
+def reference_single_core(cfg, a, om):
+    """The same compress of ONE subdomain on ONE thread (T = 1)."""
+    import oracle
+
+    secs, _ = oracle.ref().compress_batch(a[:1], om[:1], cfg.k, 1)
+    return {"value": 8.0 * cfg.m * cfg.n / secs / 1e9, "unit": "GB/s", "cores": 1, "seconds": secs,
+            "sample": f"1 subdomain ({cfg.m}x{cfg.n}) on 1 thread"}
+
+
+def repo_libraries():
+    """In-tree shared libraries mapped into this process (evidence of what ran)."""
+    libs = set()
+    try:
+        with open("/proc/self/maps") as f:
+            for line in f:
+                path = line.split()[-1] if line.strip() else ""
+                if path.startswith(ROOT) and ".so" in path:
+                    libs.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(libs)
+
+
 def run_reference(args):
-    rank, world, local = dist_env()
+    """--impl reference: rank 0 alone times the reference's own C++ on the
+    host cores; other ranks exit. Nothing here loads libspidgpu.so or torch:
+    inputs come from the CPU generator in oracle/."""
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     cfg, field, first, count = workload(args.config, 0, 1)
     threads = os.cpu_count() or 1
-    a, om = reference_inputs(cfg, field, first, count, threads, local)
+    a, om = reference_inputs(cfg, field, first, count, threads)
     vals, cpu = [], None
     for i in range(args.warmup + args.steps):
         cpu = reference_time(cfg, a, om, threads)
@@ -209,6 +294,7 @@ def run_reference(args):
             vals.append(cpu["value"])
     value = float(statistics.median(vals)) if vals else cpu["value"]
     cpu["value"] = value
+    cpu["t1"] = reference_single_core(cfg, a, om)
     nsamp = a.shape[0]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
@@ -218,9 +304,12 @@ def run_reference(args):
         "data": "synthetic",
         "config": {"workload": f"{cfg.name}: bounded sample of {nsamp} subdomains of "
                               f"{cfg.m}x{cfg.n} (k={cfg.k}, p={cfg.p}) on {threads} host threads",
-                   "subdomains": nsamp, "snapshots": cfg.n, "partition": "one subdomain per host thread"},
+                   "subdomains": nsamp, "snapshots": cfg.n, "partition": "one subdomain per host thread",
+                   "inputs": "generated on the CPU (oracle/workload.c): same field and Omega definitions"},
         "cpu_baseline": cpu,
+        "reference_class": "cpu",
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "libraries_loaded": repo_libraries(),
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -237,10 +326,12 @@ def run_ours(args):
     rank, world, local = dist_env()
     # one process per GPU; local % count only matters for the 1-GPU functional
     # check of the multi-rank path (BENCH_BACKEND=gloo), never for numbers
+    backend = os.environ.get("BENCH_BACKEND", "nccl")
+    if world > 1 and backend == "nccl" and torch.cuda.device_count() < int(os.environ.get("LOCAL_WORLD_SIZE", world)):
+        raise SystemExit(f"{world} NCCL ranks but {torch.cuda.device_count()} visible GPU(s)")
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        backend = os.environ.get("BENCH_BACKEND", "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -313,8 +404,12 @@ def run_ours(args):
         _allreduce(tm, op=dist.ReduceOp.MAX)
     ms, sk_ms = float(tm[0]), float(tm[1])
     ms_step = ms / args.steps
-    raw_local = cfg.raw_bytes(count)
-    raw_total = raw_local * world  # weak scaling: equal share per rank
+    # whole-job bytes: every rank's own count (fixed-size configs need not split evenly)
+    cnt = torch.tensor([float(count)], dtype=torch.float64, device=dev)
+    if world > 1:
+        _allreduce(cnt)
+    total_subs = int(cnt[0])
+    raw_total = cfg.raw_bytes(total_subs)
     value = raw_total / (ms_step / 1e3) / 1e9
 
     # verify phase (timed separately, after one untimed call that sizes its
@@ -389,15 +484,8 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: {count} subdomains/GPU of 32^3 x 5 QoIs x "
-                               f"{cfg.n} snapshots ({cfg.m}x{cfg.n} fp64), k={cfg.k}, p={cfg.p}, "
-                               f"in-kernel Philox Omega (discretised Gaussian Q/32); "
-                               + ("global blocks dealt round-robin over ranks, heavy = upper half of the "
-                                  "block grid" if cfg.adaptive else
-                                  f"global blocks [64r, 64r+64) on rank r (rank 0: [{first}, {first + count}))")
-                               + f" of "
-                               f"the {field.grid}^3 multimode TGV field",
-                   "subdomains": count * world, "snapshots": cfg.n,
+        "config": {"workload": describe(cfg, field, first, count, world),
+                   "subdomains": int(total_subs), "snapshots": cfg.n,
                    "partition": (f"subdomains dealt round-robin over {world} GPU(s)" if cfg.adaptive else
                                  f"static subdomain ranges over {world} GPU(s)") + ", no data exchange",
                    "l2": "inputs (21.5 GB/GPU) larger than L2 (126 MB); no flush needed"},
@@ -422,8 +510,9 @@ def run_ours(args):
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         try:
             threads = os.cpu_count() or 1
-            a_h, om_h = reference_inputs(cfg, field, first, count, threads, local, a_dev=A)
+            a_h, om_h = reference_inputs(cfg, field, first, count, threads, a_dev=A)
             line["cpu_baseline"] = reference_time(cfg, a_h, om_h, threads)
+            line["cpu_baseline"]["t1"] = reference_single_core(cfg, a_h, om_h)
         except Exception as e:  # reported, never fatal
             line["cpu_baseline"] = {"error": repr(e)}
     if rank == 0:
@@ -768,6 +857,10 @@ def pipeline_measure(cfg, A, args):
 
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch(args)
+    if not check_world(args):
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

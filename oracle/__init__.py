@@ -104,6 +104,14 @@ def _rule_args(rank, tol, kstep=None):
     return RULE_TOL, 0, float(tol), 0
 
 
+class _FieldSpec(C.Structure):
+    """orc_field_spec == spidgpu_field_spec (include/spidgpu.h)."""
+    _fields_ = [("kind", C.c_int32), ("n_modes", C.c_int32), ("grid", C.c_int64), ("block", C.c_int64),
+                ("snapshots", C.c_int64), ("t_end", C.c_double), ("nu", C.c_double), ("sigma", C.c_double),
+                ("kappa_max", C.c_double), ("mode_amp", C.c_double), ("seed", C.c_uint64),
+                ("heavy_modes", C.c_int64), ("heavy_kmin", C.c_double)]
+
+
 class _Port:
     """The C restatement (oracle/spid_oracle.c)."""
 
@@ -130,7 +138,41 @@ class _Port:
         L.orc_compression_factor.argtypes = [_sz, _sz, _sz, _D]
         L.orc_row_indices.argtypes = [_SZ, C.POINTER(C.c_int), _SZ, _sz, C.c_int, _I64, _sz, _SZ]
         L.orc_interp_apply.argtypes = [_SZ, C.POINTER(C.c_int), _SZ, _sz, C.c_int, _D, _sz, _D]
+        L.orc_omega_table.argtypes = [C.c_void_p]
+        L.orc_philox_omega.argtypes = [C.c_uint64, C.c_uint64, _sz, _sz, _sz, _D]
+        L.orc_field_generate.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, _D, C.c_int64,
+                                         C.c_int64, C.c_int]
         self.lib = L
+
+    # ---- workload generation (oracle/workload.c) -------------------------------
+    def omega_table(self) -> np.ndarray:
+        q = np.zeros(4096, dtype=np.int8)
+        self.lib.orc_omega_table(q.ctypes.data_as(C.c_void_p))
+        return q
+
+    def philox_omega(self, seed, s, ell, m, row0=0) -> np.ndarray:
+        """Omega_s rows [row0, row0+ell) as an (ell, m) Fortran array -- the
+        matrix the in-kernel Philox sketch contracts."""
+        out = np.zeros((ell, m), dtype=np.float64, order="F")
+        self.lib.orc_philox_omega(int(seed), int(s), int(row0), int(ell), int(m), _dp(out))
+        return out
+
+    def field_generate(self, spec: dict, first, batch, is_heavy=None, threads=None, out=None) -> np.ndarray:
+        """Subdomains [first, first+batch) of a BASELINE synthetic field as a
+        (batch, n, m) array (= batch column-major m x n matrices). spec holds
+        the spidgpu_field_spec fields (paper_2103_01380_b200/configs.py)."""
+        fs = _FieldSpec(**spec)
+        nq = 4 if fs.kind == 0 else 5
+        m, n = nq * fs.block ** 3, fs.snapshots
+        a = out if out is not None else np.empty((batch, n, m), dtype=np.float64)
+        hv = None
+        if is_heavy is not None:
+            hv = np.ascontiguousarray(is_heavy, dtype=np.uint8)
+        rc = self.lib.orc_field_generate(C.byref(fs), int(first), int(batch),
+                                         hv.ctypes.data_as(C.c_void_p) if hv is not None else None,
+                                         _dp(a), m, m * n, int(threads or os.cpu_count() or 1))
+        self._check(rc)
+        return a
 
     @staticmethod
     def _spec(dims, strides, periodic):

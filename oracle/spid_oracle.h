@@ -100,6 +100,30 @@ int orc_interp_apply(const size_t* dims, const int* periodic, const size_t* stri
                      int incl, const double* coarse, size_t k, double* fine);
 int orc_compression_factor(size_t m, size_t n, size_t stored, double* out); /* metrics.cpp:5-12 */
 
+/* ---- workload generation (oracle/workload.c): the bench inputs on the CPU,
+ * for the reference arm, which must not load the product library. ---- */
+
+/* The 4096-entry quantile table Q of the discretised N(0,1) (Omega = Q/32). */
+void orc_omega_table(int8_t* q);
+/* Omega_s rows [row0, row0+ell) x m columns (ell x m, column-major): the
+ * performance-mode sketch matrix (Philox4x32-7). */
+void orc_philox_omega(uint64_t seed, uint64_t s, size_t row0, size_t ell, size_t m, double* out);
+
+/* Same layout as spidgpu_field_spec (include/spidgpu.h). */
+typedef struct orc_field_spec {
+    int32_t kind; /* 0 TGV4, 1 TGV5, 2 MULTIMODE */
+    int32_t n_modes;
+    int64_t grid, block, snapshots;
+    double t_end, nu, sigma, kappa_max, mode_amp;
+    uint64_t seed;
+    int64_t heavy_modes;
+    double heavy_kmin;
+} orc_field_spec;
+/* Subdomains [first, first+batch) of the BASELINE synthetic fields (m x n
+ * each, ld lda, stride strideA), on `threads` host threads. */
+int orc_field_generate(const orc_field_spec* spec, int64_t first, int64_t batch, const uint8_t* is_heavy,
+                       double* A, int64_t lda, int64_t strideA, int threads);
+
 #ifdef __cplusplus
 }
 #endif
