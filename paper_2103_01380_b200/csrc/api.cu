@@ -103,17 +103,21 @@ int do_sketch(spidgpu_handle h, Workspace& ws, const double* A, int64_t m, int64
     // HBM-bound); explicit Omega (arbitrary fp64 entries) and
     // SPIDGPU_OPT_DMMA_SKETCH: the DMMA kernel
     const bool tc = om->mode == SPIDGPU_OMEGA_PHILOX && !h->force_dmma_sketch;
+    const int sms = h->sketch_sms > 0 ? h->sketch_sms : h->num_sms;
     int64_t slice = tc ? kSketchTcMaxEll : 80;
+    if (tc && ell > 64 && ell <= 80) {
+        // one pass as a slice-split CTA pair when clusters are available
+        SketchPlan probe;
+        if (!sketch_tc_make_plan(m, n, batch, ell, sms, h->sketch_pairs, h->sketch_seg_rows, &probe)) slice = 64;
+    }
     if (tc && ell > slice) {
-        // even passes of whole 16-row groups: ell = 80 runs as 48 + 32, not 64 + 16
-        // (the Omega/MMA work per A pass grows with the pass width)
+        // even passes of whole 16-row groups (ell = 100 runs as 64 + 36 -> 50 + 50)
         const int64_t passes = (ell + slice - 1) / slice;
-        slice = std::min<int64_t>(16 * (((ell + passes - 1) / passes + 15) / 16), kSketchTcMaxEll);
+        slice = std::min<int64_t>(16 * (((ell + passes - 1) / passes + 15) / 16), slice);
     }
     for (int64_t row0 = 0; row0 < ell; row0 += slice) {
         const int64_t ells = std::min<int64_t>(slice, ell - row0);
         SketchPlan plan;
-        const int sms = h->sketch_sms > 0 ? h->sketch_sms : h->num_sms;
         const bool planned = tc ? sketch_tc_make_plan(m, n, batch, ells, sms, h->sketch_pairs, h->sketch_seg_rows, &plan)
                                 : sketch_make_plan(m, n, batch, ells, sms, &plan);
         if (!planned) return fail(h, SPID_SHAPE_UNSUPPORTED, "no sketch plan");

@@ -75,7 +75,7 @@ struct SketchPlan {
     int64_t total_units;  // batch * (ntiles_col / (1 + pair)) * nseg
     int grid;             // CTAs (persistent, contiguous ranges of whole units)
     int halves = 1;       // partial tiles per slot (2: slice halves of a split CTA pair)
-    int pair = 0;         // 1: CTAs run as clusters of two over column-tile pairs (sketch_tc.cu)
+    int pair = 0;         // sketch_tc.cu cluster mode: 0 none, 1 column-tile pairs, 2 slice-split pairs
     size_t smem;
     size_t partial_elems; // doubles of the partial workspace: batch*ntiles_col*nseg*halves*ell_pad*nt
 };
@@ -104,7 +104,7 @@ cudaError_t launch_sketch(const SketchParams& p, const SketchPlan& plan, const C
 // fixed-order reduction of the segment partials into Y (both sketch kernels)
 cudaError_t launch_sketch_reduce(const SketchParams& p, const SketchPlan& plan, cudaStream_t stream);
 // the exact integer-sliced sketch on tcgen05.mma kind::i8 with TMEM accumulators (sketch_tc.cu)
-constexpr int64_t kSketchTcMaxEll = 64;
+constexpr int64_t kSketchTcMaxEll = 80;
 // seg_rows: rows per segment (0 = kSketchSegRows; a multiple of 512, <= 65536)
 bool sketch_tc_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int num_sms, int pair_mode,
                          int64_t seg_rows, SketchPlan* plan);

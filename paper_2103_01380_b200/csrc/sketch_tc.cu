@@ -87,25 +87,57 @@ constexpr int kBoxBytes = 16 * kM * 8;              // 16 rows x 128 columns fp6
 constexpr int kAStageBytes = 2 * kBoxBytes;         // 32 KB
 constexpr int kAStages = 5;
 constexpr int kSliceBytes = kM * kRows;             // 4 KB per slice tile
-constexpr int kBStages = 2;
 
 // instrumentation (spidgpu_debug_counters): converter-warp flushes by cause
 // [segment end, headroom overflow, magnitude fallback]; atomics only on flushes
 __device__ unsigned long long g_tc_flushes[3];
 
-template <int NPAD>
+// Kernel modes. 0: one CTA per (subdomain, 128-column tile). 1 (tile pair):
+// clusters of two over a subdomain's two column tiles, sharing each stage's
+// Omega tile. 2 (slice split): clusters of two over the SAME column tile, so
+// that ell_pad = 80 fits TMEM (8 accumulators x 80 columns would not fit 512):
+//   - CTA r loads and converts only rows [16r, 16r + 16) of every 32-row
+//     stage -- exactly K half r of every slice tile -- so A is read and
+//     converted once;
+//   - a column's exponent must be the same in both CTAs: each publishes its
+//     16-row column maxima into the peer's mailbox (st.async, one stage
+//     ahead of use) and both take the max of the two halves, so both make
+//     identical epoch decisions;
+//   - CTA 0 keeps slices 0-3, CTA 1 slices 4-6 and the offset accumulator
+//     (4 accumulators of N = 80 each); the slices a CTA does not keep go to
+//     the peer's slice tiles by st.async, counted on its stage barrier;
+//   - each CTA flushes its own accumulators into its half of the segment's
+//     partial slot (the reduction adds the halves).
+// The single-pass sketch for ell in (64, 80] (config 4's kmax 64 + p 16).
+template <int NPAD, int MODE>
 struct TcCfg {
-    static constexpr int kOmegaBytes = NPAD * kRows;
-    static constexpr int kBStageBytes = kSlices * kSliceBytes + kOmegaBytes;
+    static constexpr bool kSplit = MODE == 2;
+    static constexpr int kSl = kSplit ? 4 : kSlices;        // slice tiles per B stage
+    static constexpr int kAcc = kSplit ? 4 : kSlices + 1;   // TMEM accumulators
+    // rows per stage: 32 (one UMMA K block); split: 64, 32 per CTA, so each
+    // converter thread still handles 16 entries per stage and the per-stage
+    // costs (barriers, exponent checks) are paid once per 64 rows
+    static constexpr int kStageRows = kSplit ? 64 : kRows;
+    static constexpr int kKB = kStageRows / kRows;            // UMMA K blocks per stage
+    static constexpr int kTileBytes = kKB * kSliceBytes;      // one slice tile of a stage
+    static constexpr int kOmegaBytes = NPAD * kStageRows;
+    static constexpr int kBStageBytes = kSl * kTileBytes + kOmegaBytes;
+    // slice/Omega stages: 2 (3 in split mode, whose two CTAs advance in lock-step)
+    static constexpr int kBStages = kSplit ? 2 : 2;
+    // A ring: 2 x 16-row boxes per stage (split: this CTA's 32 rows of the 64)
+    static constexpr int kAStB = kAStageBytes;
+    static constexpr int kASt = kSplit ? 4 : kAStages;
+    static_assert(!kSplit || kASt >= 3, "mailbox slots outlive the peer lead");
     // D_0..D_6 (slices) and D_7 = sum_k Q (all-ones A tile): the offset correction
-    static constexpr int kTmemCols = (kSlices + 1) * NPAD <= 256 ? 256 : 512;
+    static constexpr int kTmemCols = kAcc * NPAD <= 256 ? 256 : 512;
+    static_assert(kAcc * NPAD <= 512, "TMEM columns");
     // layout: A ring | B ring | ebx[2][128] | flags | barriers
-    static constexpr size_t kOffB = static_cast<size_t>(kAStages) * kAStageBytes;
+    static constexpr size_t kOffB = static_cast<size_t>(kASt) * kAStB;
     static constexpr size_t kOffMisc = kOffB + static_cast<size_t>(kBStages) * kBStageBytes;
-    // Omega table; TMEM slot; all-ones core matrix
-    static constexpr size_t kMiscBytes = 4096 + 64 + 128;
+    // Omega table; TMEM slot; all-ones core matrix; (split) the peer's column maxima per A slot
+    static constexpr size_t kMiscBytes = 4096 + 64 + 128 + (kSplit ? kASt * kM * 4 : 0);
     static constexpr size_t kOffBar = (kOffMisc + kMiscBytes + 7) & ~size_t(7);
-    static constexpr size_t kSmem = 1024 + kOffBar + 8 * (2 * kAStages + 2 * kBStages) + 16;
+    static constexpr size_t kSmem = 1024 + kOffBar + 8 * (3 * kASt + 2 * kBStages) + 16;
 };
 
 struct ChunkPos {
@@ -197,6 +229,11 @@ __device__ __forceinline__ void st_async_v4(uint32_t raddr, uint32_t a, uint32_t
         "r"(a), "r"(b), "r"(c), "r"(d), "r"(rbar)
         : "memory");
 }
+__device__ __forceinline__ void st_async_b32(uint32_t raddr, uint32_t a, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];\n" ::"r"(raddr), "r"(a),
+                 "r"(rbar)
+                 : "memory");
+}
 __device__ __forceinline__ void st_async_v2(uint32_t raddr, uint32_t a, uint32_t b, uint32_t rbar) {
     asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];\n" ::"r"(raddr),
                  "r"(a), "r"(b), "r"(rbar)
@@ -248,32 +285,38 @@ __device__ __forceinline__ double2 unfix_scale(int eb) {
 // of line: flushes are rare (segment ends, exponent restarts), and inlining
 // their 8 x 8 TMEM loads into the converter loop raised its register
 // pressure enough for the compiler to rematerialise addresses every stage.
-template <int NPAD>
+// Split mode (MODE 2): CTA 0 holds D_0..D_3 and writes lo * 2^(E-P-5);
+// CTA 1 holds D_4..D_6 and D_7 and writes hi * 2^32 * 2^(E-P-5), each into
+// its half of the segment's slot (the reduction adds the halves).
+template <int NPAD, int MODE>
 __device__ __noinline__ void tc_flush_rows(uint32_t taddr, double* part, int ebf, int psf, int pf, int col_f,
-                                           bool final_flush, bool zero, bool first) {
+                                           bool final_flush, bool zero, bool first, int half) {
+    constexpr int kAcc = TcCfg<NPAD, MODE>::kAcc;
     const double2 u = unfix_scale(ebf);
 #pragma unroll 1
     for (int g0 = 0; g0 < NPAD; g0 += 16) {
         // exact: sum_t 2^(8t) D_t - kOffset * D_7 as hi * 2^32 + lo, for
         // columns g0 + pf + 2j of this thread's D row
-        uint32_t v[kSlices + 1][8];
+        uint32_t v[kAcc][8];
 #pragma unroll
-        for (int t = 0; t <= kSlices; ++t) tmem_ld16x64b_x8(taddr + NPAD * t + g0, v[t]);
+        for (int t = 0; t < kAcc; ++t) tmem_ld16x64b_x8(taddr + NPAD * t + g0, v[t]);
         tmem_ld_wait();
         if (zero) {
 #pragma unroll
-            for (int t = 0; t <= kSlices; ++t) tmem_st16x64b_x8_zero(taddr + NPAD * t + g0);
+            for (int t = 0; t < kAcc; ++t) tmem_st16x64b_x8_zero(taddr + NPAD * t + g0);
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             long long lo64 = 0, hi64 = 0;
 #pragma unroll
-            for (int t = 0; t <= kSlices; ++t) {
+            for (int t = 0; t < kAcc; ++t) {
                 const long long d = static_cast<int>(v[t][j]);
-                if (t < 4)
-                    lo64 += d * (1LL << (8 * t));
-                else if (t < kSlices)
-                    hi64 += d * (1LL << (8 * (t - 4)));
+                // slice index of accumulator t (split: CTA 1's are slices 4.. and the offset)
+                const int sl = MODE == 2 ? t + 4 * half : t;
+                if (sl < 4)
+                    lo64 += d * (1LL << (8 * sl));
+                else if (sl < kSlices)
+                    hi64 += d * (1LL << (8 * (sl - 4)));
                 else
                     hi64 -= d * kOffsetHi;
             }
@@ -286,21 +329,28 @@ __device__ __noinline__ void tc_flush_rows(uint32_t taddr, double* part, int ebf
     if (zero) tmem_st_wait();
 }
 
-// kPair: the CTAs run as clusters of two that sketch the two column tiles
-// (128 snapshots each) of the same subdomain over the same 32-row stages, so
-// each generates HALF of every stage's Omega tile and writes it into both
-// CTAs' shared memory (the peer's half arrives by st.async, counted on the
-// local stage barrier as transaction bytes); every MMA completion is
-// multicast to both CTAs' slot barriers, so a slot is refilled only when
-// both CTAs' MMAs have read it. The stream-K partition runs over pair units
-// (subdomain, column-tile pair, stage); ntiles_u = column tiles per
-// subdomain / (1 + kPair).
-template <int NPAD, bool kPair>
+// Clusters (modes 1 and 2): each CTA generates HALF of every stage's Omega
+// tile and writes it into both CTAs' shared memory (the peer's half arrives
+// by st.async, counted on the local stage barrier as transaction bytes);
+// every MMA completion is multicast to both CTAs' slot barriers, so a slot is
+// refilled only when both CTAs' MMAs have read it. Work units are (subdomain,
+// column tile -- or tile pair in mode 1 --, segment); ntiles_col counts
+// units' column tiles (column tiles / 2 in mode 1).
+template <int NPAD, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchParams p, int64_t nchunk,
                      int64_t ntiles_col, int64_t nseg, int64_t seg_len, int64_t total_units) {
-    constexpr int P = kPair ? 2 : 1;
-    using Cfg = TcCfg<NPAD>;
+    constexpr bool kPair = MODE != 0;             // a cluster of two
+    constexpr bool kSplit = MODE == 2;
+    constexpr int P = kPair ? 2 : 1;              // CTAs per work-unit owner
+    constexpr int TP = MODE == 1 ? 2 : 1;         // column tiles per unit
+    constexpr int kHalves = kSplit ? 2 : 1;       // partials per segment slot
+    using Cfg = TcCfg<NPAD, MODE>;
+    constexpr int kSl = Cfg::kSl;
+    constexpr int kBStages = Cfg::kBStages;
+    constexpr int kAStages = Cfg::kASt;
+    constexpr int kAStageBytes = Cfg::kAStB;
+    constexpr int kStageRows = Cfg::kStageRows, kKB = Cfg::kKB, kTileBytes = Cfg::kTileBytes;
     extern __shared__ unsigned char smem_raw[];
     const uint32_t raw_s = smem_u32(smem_raw);
     const uint32_t base_s = (raw_s + 1023u) & ~1023u;
@@ -311,10 +361,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tab + 4096);
     // one all-ones 8x16 core matrix; with LBO = SBO = 0 it reads as a 128 x 32 all-ones A tile
     const uint32_t ones_s = smem_u32(tab + 4096 + 64);
+    const uint32_t mbox_s = smem_u32(tab + 4096 + 64 + 128);  // split: [kAStages][kM] peer maxima
     uint64_t* a_full = reinterpret_cast<uint64_t*>(base + Cfg::kOffBar);
     uint64_t* a_empty = a_full + kAStages;
     uint64_t* b_full = a_empty + kAStages;
     uint64_t* b_empty = b_full + kBStages;
+    uint64_t* m_full = b_empty + kBStages;  // split: the peer's maxima of an A slot arrived
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t c = blockIdx.x;
@@ -334,7 +386,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < kAStages; ++i) {
             mbar_init(&a_full[i], 1);
             mbar_init(&a_empty[i], kConvWarps);
+            mbar_init(&m_full[i], 1);
         }
+        if constexpr (kSplit)  // the mailboxes' first phases: the peer's 128 column maxima of stages 0..
+            for (int i = 0; i < kAStages; ++i) mbar_arrive_expect_tx(&m_full[i], kM * 4);
         for (int i = 0; i < kBStages; ++i) {
             mbar_init(&b_full[i], kConvWarps + kGenWarps);
             mbar_init(&b_empty[i], P);  // MMA commits of this CTA (and of its peer)
@@ -365,8 +420,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // most one task per stage, so the tile's latency is one task's.
         // A pair splits the tile's tasks: this CTA runs [rank, rank + 1) x
         // kTasksCta of them and also writes them into the peer's tile.
-        constexpr bool kFine = 4 * NPAD <= 32 * kGenWarps * P;
-        constexpr int kTasks = kFine ? 4 * NPAD : 2 * NPAD;
+        constexpr int kOctets = kStageRows / 8;  // per Omega row and stage
+        constexpr bool kFine = kOctets * NPAD <= 32 * kGenWarps * P;
+        constexpr int kTasks = kFine ? kOctets * NPAD : kOctets / 2 * NPAD;
         constexpr int kTasksCta = kTasks / P;
         constexpr int kTasksPerWarp = (kTasksCta + kGenWarps - 1) / kGenWarps;
         constexpr uint32_t kPeerBytes = kTasksCta * (kFine ? 8 : 16);  // Omega bytes the peer sends per stage
@@ -385,11 +441,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             // zero their rows themselves
             const uint32_t acc = seg_pos != 0 ? 1u : 0u;
             const uint32_t st = b_s + sl * Cfg::kBStageBytes;
-            const uint64_t bdesc = smem_desc(st + kSlices * kSliceBytes, NPAD * 16, 128);
+            const uint32_t ot = st + kSl * kTileBytes;  // Omega tile: K blocks of NPAD x 32 bytes
+            if constexpr (!kSplit) {
+                const uint64_t bdesc = smem_desc(ot, NPAD * 16, 128);
 #pragma unroll
-            for (int t = 0; t < kSlices; ++t)
-                umma_i8(tmem + NPAD * t, smem_desc(st + t * kSliceBytes, kM * 16, 128), bdesc, kIdU, acc);
-            umma_i8(tmem + NPAD * kSlices, ones_desc, bdesc, kIdU, acc);
+                for (int t = 0; t < kSlices; ++t)
+                    umma_i8(tmem + NPAD * t, smem_desc(st + t * kTileBytes, kM * 16, 128), bdesc, kIdU, acc);
+                umma_i8(tmem + NPAD * kSlices, ones_desc, bdesc, kIdU, acc);
+            } else {
+                // CTA 0: slices 0-3; CTA 1: slices 4-6 (tiles 0-2) and the offset
+                // (ones); one MMA per K block (K block kb = rows of CTA kb)
+#pragma unroll
+                for (int kb = 0; kb < kKB; ++kb) {
+                    const uint64_t bdesc = smem_desc(ot + kb * (NPAD * 32), NPAD * 16, 128);
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        umma_i8(tmem + NPAD * t,
+                                rank == 1 && t == 3 ? ones_desc
+                                                    : smem_desc(st + t * kTileBytes + kb * kSliceBytes, kM * 16, 128),
+                                bdesc, kIdU, kb > 0 ? 1u : acc);
+                }
+            }
             if constexpr (kPair)
                 umma_commit_pair(&b_empty[sl]);
             else
@@ -400,11 +472,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto issue_tma = [&](int it) {
             const int sl = it % kAStages;
             mbar_arrive_expect_tx(&a_full[sl], kAStageBytes);
+            // two 16-row boxes: the stage's 32 rows (split: this CTA's 32 of the 64)
 #pragma unroll
             for (int b = 0; b < 2; ++b)
                 tma_load_3d(base + sl * kAStageBytes + b * kBoxBytes, &tmap, &a_full[sl],
-                            static_cast<int>(tp.kc * kRows + 16 * b),
-                            static_cast<int>((tp.ct * P + static_cast<int>(rank)) * kM),
+                            static_cast<int>(tp.kc * kStageRows + (kSplit ? 32 * static_cast<int>(rank) : 0) + 16 * b),
+                            static_cast<int>((tp.ct * TP + (TP == 2 ? static_cast<int>(rank) : 0)) * kM),
                             static_cast<int>(tp.s));
             advance(tp, static_cast<int>(nchunk), static_cast<int>(ntiles_col));
         };
@@ -424,8 +497,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else
         for (int it = 0; it < niter; ++it) {
             const int sl = it % kBStages;
-            const uint32_t ot = b_s + sl * Cfg::kBStageBytes + kSlices * kSliceBytes;
-            const uint32_t ko = static_cast<uint32_t>((cp.kc * kRows) >> 3);
+            const uint32_t ot = b_s + sl * Cfg::kBStageBytes + kSl * kTileBytes;
+            const uint32_t ko = static_cast<uint32_t>((cp.kc * kStageRows) >> 3);
             const int task_l = gw * kTasksPerWarp + lane;
             const bool has_task = lane < kTasksPerWarp && task_l < kTasksCta;
             const int task = static_cast<int>(rank) * kTasksCta + task_l;
@@ -465,8 +538,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) {
-                if (kPair && warp == 0)
-                    mbar_arrive_expect_tx(&b_full[sl], kPeerBytes);  // the peer's half of the tile
+                if (kPair && warp == 0)  // the peer's half of the Omega tile (and, split, its K half of our slices)
+                    mbar_arrive_expect_tx(&b_full[sl], kPeerBytes + (kSplit ? (rank == 0 ? 4u : 3u) * kSliceBytes : 0u));
                 else
                     mbar_arrive(&b_full[sl]);
             }
@@ -505,8 +578,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         bool pending = false;  // this warp's D rows hold unflushed stages
         // partial slot of the current segment (absolute: (tile, segment));
         // pre-decremented so the first segment start lands on it
-        int seg_slot = static_cast<int>((static_cast<int64_t>(cp.s) * ntiles_col * P + cp.ct * P + rank) * nseg +
-                                        cp.kc / seg_len) - 1;
+        int seg_slot = static_cast<int>((static_cast<int64_t>(cp.s) * ntiles_col * TP + cp.ct * TP +
+                                         (TP == 2 ? rank : 0)) * nseg + cp.kc / seg_len) - 1;
         bool seg_first = true; // its first flush stores, later ones add
         int seg_left = 0;      // stages left in the current segment (ranges start on segment starts)
         const int nch = static_cast<int>(nchunk), ntc = static_cast<int>(ntiles_col);
@@ -518,39 +591,71 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto flush = [&](int it_last, bool final_flush, bool zero) {
             mbar_wait(&b_empty[it_last % kBStages], (it_last / kBStages) & 1);  // MMAs <= it_last done
             tc_fence_after();
-            tc_flush_rows<NPAD>(tmem + lane_base, p.partial + static_cast<int64_t>(seg_slot) * (NPAD * kM),
-                                __shfl_sync(0xffffffffu, eb, lf),  // lane lf converts column lf (b = 0)
-                                __shfl_sync(0xffffffffu, poison, lf), pf, col_f, final_flush, zero, seg_first);
+            const int half = kSplit ? static_cast<int>(rank) : 0;
+            tc_flush_rows<NPAD, MODE>(tmem + lane_base,
+                                      p.partial + (static_cast<int64_t>(seg_slot) * kHalves + half) * (NPAD * kM),
+                                      __shfl_sync(0xffffffffu, eb, lf),  // lane lf converts column lf (b = 0)
+                                      __shfl_sync(0xffffffffu, poison, lf), pf, col_f, final_flush, zero, seg_first,
+                                      half);
             tc_fence_before();
         };
 
-        // rows [16 b, 16 b + 16) of column col of stage it: 8 conflict-free 16B loads
-        auto load = [&](int it, double (&xv)[16]) {
+        // 16 entries per converter thread per stage: rows [16 b, 16 b + 16) of
+        // column col of this CTA's 32 rows
+        constexpr int kEnt = 16;
+        auto load = [&](int it, double (&xv)[kEnt]) {
             const int sa = it % kAStages;
             mbar_wait(&a_full[sa], (it / kAStages) & 1);
+            // 128B-swizzled box rows: column col is 128 B (16 rows) per box
             const uint32_t cb = a_s + sa * kAStageBytes + b * kBoxBytes + col * 128;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < kEnt / 2; ++j) {
                 const double2 v = lds128(cb + ((j ^ (col & 7)) << 4));
                 xv[2 * j] = v.x;
                 xv[2 * j + 1] = v.y;
             }
         };
-        // column max |x| high word over both row halves; using it also
-        // completes the loads, so the A slot goes back to the TMA refill
-        auto col_max = [&](int it, const double (&xv)[16]) {
+        // column max |x| high word over both row halves (split: over this
+        // CTA's 16 rows, published to the peer); using it also completes the
+        // loads, so the A slot goes back to the TMA refill
+        auto col_max = [&](int it, const double (&xv)[kEnt]) {
             uint32_t mx = 0;
 #pragma unroll
-            for (int e = 0; e < 16; ++e) mx = max(mx, static_cast<uint32_t>(__double2hiint(xv[e])) & 0x7fffffffu);
+            for (int e = 0; e < kEnt; ++e) mx = max(mx, static_cast<uint32_t>(__double2hiint(xv[e])) & 0x7fffffffu);
             mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+            if constexpr (kSplit) {
+                if (b == 0) {
+                    const int sa = it % kAStages;
+                    st_async_b32(peer_addr(mbox_s + (sa * kM + col) * 4, rank ^ 1u), mx,
+                                 peer_addr(smem_u32(&m_full[sa]), rank ^ 1u));
+                }
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive(&a_empty[it % kAStages]);
             return mx;
         };
+        // split: the whole column's maximum = max(ours, the peer's), read
+        // a stage after it was published
+        auto peer_max = [&](int it, uint32_t mx) -> uint32_t {
+            if constexpr (kSplit) {
+                const int sa = it % kAStages;
+                mbar_wait(&m_full[sa], (it / kAStages) & 1);
+                uint32_t pm;
+                asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(pm) : "r"(mbox_s + (sa * kM + col) * 4));
+                // re-arm the slot for stage it + kAStages once this phase is
+                // complete (this thread just saw it complete); the peer writes
+                // that stage's maxima only a few stages later (B-ring lock-step)
+                if (warp == 8 && lane == 0) mbar_arrive_expect_tx(&m_full[sa], kM * 4);
+                return max(mx, pm);
+            } else {
+                return mx;
+            }
+        };
 
-        auto step = [&](int it, const double (&xc)[16], uint32_t mx, double (&xn)[16]) -> uint32_t {
+        auto step = [&](int it, const double (&xc)[kEnt], uint32_t mx, double (&xn)[kEnt]) -> uint32_t {
             const int sb = it % kBStages;
             const bool new_seg = seg_left == 0;
+            mx = peer_max(it, mx);
             if (__any_sync(0xffffffffu, new_seg || mx >= thr || mx < thr_lo)) {  // warp-uniform, rare
                 const bool over = __any_sync(0xffffffffu, mx >= thr);
                 if (pending) {
@@ -563,7 +668,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (new_seg) {
                     // tiles follow each other in the flat order, each nseg slots
                     // wide; a pair's CTAs skip their peer's tile
-                    seg_slot += (cp.kc == 0 && pending) ? 1 + (P - 1) * static_cast<int>(nseg) : 1;
+                    seg_slot += (cp.kc == 0 && pending) ? 1 + (TP - 1) * static_cast<int>(nseg) : 1;
                     seg_first = true;
                     poison = 0;
                     seg_left = min(static_cast<int>(seg_len), nch - cp.kc);
@@ -583,25 +688,31 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             --seg_left;
             const bool more = it + 1 < niter;
-            if (more) load(it + 1, xn);
+            uint32_t mxn = 0;
+            if (more) {
+                load(it + 1, xn);
+                if constexpr (kSplit) mxn = col_max(it + 1, xn);  // published a stage ahead of use
+            }
             // one DFMA per entry -- t = RN(x 2^(P-E) + 1.5 2^52), whose low 56
             // bits are u = rint(x 2^(P-E)) + kOffset -- then 4x4 PRMT byte
-            // transposes and one 16-byte store per slice (K half b, row col).
+            // transposes and one 16-byte store per slice (K half b, row col;
+            // split: of K block rank).
             // The rare two-factor scale (tiny columns) is a separate copy of
             // the whole emit path, so the hot path has no register joins.
-            const uint32_t st = b_s + sb * Cfg::kBStageBytes + b * (kM * 16) + col * 16;
+            const uint32_t st = b_s + sb * Cfg::kBStageBytes + (kSplit ? rank * kSliceBytes : 0) + b * (kM * 16) +
+                                col * 16;
             auto emit = [&](auto two_factor) {
-                uint32_t lw[16], hw[16];
+                uint32_t lw[kEnt], hw[kEnt];
 #pragma unroll
-                for (int e = 0; e < 16; ++e) {
+                for (int e = 0; e < kEnt; ++e) {
                     const double t = decltype(two_factor)::value ? fma(xc[e] * sclx, scly, kMagic)
                                                                  : fma(xc[e], sclx, kMagic);
                     hw[e] = static_cast<uint32_t>(__double2hiint(t));
                     lw[e] = static_cast<uint32_t>(__double2loint(t));
                 }
-                uint32_t sw[kSlices][4];
+                uint32_t sw[kSlices][kEnt / 4];
 #pragma unroll
-                for (int g4 = 0; g4 < 4; ++g4) {
+                for (int g4 = 0; g4 < kEnt / 4; ++g4) {
                     const uint32_t* wl = lw + 4 * g4;
                     const uint32_t* wh = hw + 4 * g4;
                     {
@@ -620,11 +731,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                         sw[6][g4] = __byte_perm(t1, t3, 0x5410);
                     }
                 }
-                // the slice slot is free once the MMAs that read it completed:
-                // only the stores wait, the conversion runs ahead
+                // the slice slot is free once the MMAs that read it completed
+                // (split: both CTAs' MMAs, the commits are multicast): only
+                // the stores wait, the conversion runs ahead
                 if (it >= kBStages) mbar_wait(&b_empty[sb], ((it / kBStages) - 1) & 1);
+                if constexpr (!kSplit) {
 #pragma unroll
-                for (int t = 0; t < kSlices; ++t) sts128u(st + t * kSliceBytes, sw[t][0], sw[t][1], sw[t][2], sw[t][3]);
+                    for (int t = 0; t < kSlices; ++t)
+                        sts128u(st + t * kTileBytes, sw[t][0], sw[t][1], sw[t][2], sw[t][3]);
+                } else {
+                    // CTA 0 keeps slices 0-3 (tiles 0-3), CTA 1 slices 4-6 (tiles
+                    // 0-2); the other CTA's slices go to its tiles at the same
+                    // offset, counted on its stage barrier
+                    const uint32_t peer = rank ^ 1u;
+                    const uint32_t rbar = peer_addr(smem_u32(&b_full[sb]), peer);
+                    if (rank == 0) {
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) sts128u(st + t * kTileBytes, sw[t][0], sw[t][1], sw[t][2], sw[t][3]);
+#pragma unroll
+                        for (int t = 4; t < kSlices; ++t)
+                            st_async_v4(peer_addr(st + (t - 4) * kTileBytes, peer), sw[t][0], sw[t][1], sw[t][2], sw[t][3],
+                                        rbar);
+                    } else {
+#pragma unroll
+                        for (int t = 4; t < kSlices; ++t)
+                            sts128u(st + (t - 4) * kTileBytes, sw[t][0], sw[t][1], sw[t][2], sw[t][3]);
+#pragma unroll
+                        for (int t = 0; t < 4; ++t)
+                            st_async_v4(peer_addr(st + t * kTileBytes, peer), sw[t][0], sw[t][1], sw[t][2], sw[t][3], rbar);
+                    }
+                }
             };
             if (!tiny)
                 emit(std::false_type{});
@@ -635,10 +771,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) mbar_arrive(&b_full[sb]);
             pending = true;
             advance(cp, nch, ntc);
-            return more ? col_max(it + 1, xn) : 0u;
+            if constexpr (kSplit)
+                return mxn;
+            else
+                return more ? col_max(it + 1, xn) : 0u;
         };
 
-        double xa[16], xb[16];
+        double xa[kEnt], xb[kEnt];
         load(0, xa);
         uint32_t mx = col_max(0, xa);
         for (int it = 0; it < niter; it += 2) {
@@ -658,15 +797,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-template <int NPAD, bool kPair>
+template <int NPAD, int MODE>
 cudaError_t launch_t(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap, cudaStream_t stream) {
-    using Cfg = TcCfg<NPAD>;
+    using Cfg = TcCfg<NPAD, MODE>;
     static_assert(Cfg::kSmem <= 227 * 1024, "shared memory budget");
-    auto kern = sketch_tc_kernel<NPAD, kPair>;
+    auto kern = sketch_tc_kernel<NPAD, MODE>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::kSmem));
     if (e != cudaSuccess) return e;
-    const int64_t ntiles_u = plan.ntiles_col / (kPair ? 2 : 1);
-    if constexpr (kPair) {
+    const int64_t ntiles_u = plan.ntiles_col / (MODE == 1 ? 2 : 1);
+    if constexpr (MODE != 0) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(static_cast<unsigned>(plan.grid));
         cfg.blockDim = dim3(kThreads);
@@ -691,14 +830,14 @@ cudaError_t launch_t(const SketchParams& p, const SketchPlan& plan, const CUtens
 }
 
 // CTA pairs the device keeps resident at once for this kernel (0 if clusters
-// of two cannot be launched); cached per ell_pad for the process's device
-// (one GPU per process; a racing first call computes the same value)
-template <int NPAD>
+// of two cannot be launched); cached per (ell_pad, mode) for the process's
+// device (one GPU per process; a racing first call computes the same value)
+template <int NPAD, int MODE>
 int max_pairs() {
     static int cached = -1;
     if (cached >= 0) return cached;
-    using Cfg = TcCfg<NPAD>;
-    auto kern = sketch_tc_kernel<NPAD, true>;
+    using Cfg = TcCfg<NPAD, MODE>;
+    auto kern = sketch_tc_kernel<NPAD, MODE>;
     int n = 0;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::kSmem)) ==
         cudaSuccess) {
@@ -720,12 +859,13 @@ int max_pairs() {
     return n;
 }
 
-int max_pairs_for(int ell_pad) {
+int max_pairs_for(int ell_pad, int mode) {
+    if (mode == 2) return ell_pad == 80 ? max_pairs<80, 2>() : 0;
     switch (ell_pad) {
-        case 16: return max_pairs<16>();
-        case 32: return max_pairs<32>();
-        case 48: return max_pairs<48>();
-        case 64: return max_pairs<64>();
+        case 16: return max_pairs<16, 1>();
+        case 32: return max_pairs<32, 1>();
+        case 48: return max_pairs<48, 1>();
+        case 64: return max_pairs<64, 1>();
         default: return 0;
     }
 }
@@ -751,46 +891,63 @@ bool sketch_tc_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int n
     plan->nw = 1;
     plan->nt = kM;
     plan->ntiles_col = (n + kM - 1) / kM;
-    plan->kc_rows = kRows;
-    plan->nchunk = (m + kRows - 1) / kRows;
-    // CTA pairs when the column tiles pair up and the device keeps at least
-    // as many pairs resident as half the SM budget (clusters of two span a
-    // TPC). pair_mode 1 (default) pairs only ell_pad 64, where halving the
-    // Omega work outweighs the pair's lock-step (base clock, config 3: -3% at
-    // 64, +4.5% at 48, +8% at 16); 2 pairs whenever possible (tests, A/B).
-    const bool want = pair_mode == 2 || (pair_mode == 1 && plan->ell_pad == 64);
-    const int pairs = want && num_sms >= 2 && plan->ntiles_col % 2 == 0 ? max_pairs_for(plan->ell_pad) : 0;
-    plan->pair = pairs > 0 && 2 * pairs >= num_sms - 1 ? 1 : 0;
+    plan->kc_rows = kRows;  // set per mode below
+    // ell_pad 80: the slice-split pair (mode 2), the only mode whose TMEM
+    // fits 80 columns per accumulator; without clusters the caller splits
+    // the sketch into passes of <= 64 rows instead.
+    // Otherwise CTA pairs (mode 1) when the column tiles pair up and the
+    // device keeps at least as many pairs resident as half the SM budget
+    // (clusters of two span a TPC). pair_mode 1 (default) pairs only ell_pad
+    // 64, where halving the Omega work outweighs the pair's lock-step (base
+    // clock, config 3: -3% at 64, +4.5% at 48, +8% at 16); 2 pairs whenever
+    // possible (tests, A/B).
+    int pairs = 0;
+    if (plan->ell_pad == 80) {
+        pairs = num_sms >= 2 ? max_pairs_for(80, 2) : 0;
+        if (pairs == 0) return false;
+        plan->pair = 2;
+    } else {
+        const bool want = pair_mode == 2 || (pair_mode == 1 && plan->ell_pad == 64);
+        pairs = want && num_sms >= 2 && plan->ntiles_col % 2 == 0 ? max_pairs_for(plan->ell_pad, 1) : 0;
+        plan->pair = pairs > 0 && 2 * pairs >= num_sms - 1 ? 1 : 0;
+    }
     const int P = plan->pair ? 2 : 1;
-    plan->seg_len = (seg_rows > 0 ? seg_rows : kSketchSegRows) / kRows;
+    const int TP = plan->pair == 1 ? 2 : 1;
+    plan->kc_rows = plan->pair == 2 ? 2 * kRows : kRows;  // split stages: 64 rows, 32 per CTA
+    plan->nchunk = (m + plan->kc_rows - 1) / plan->kc_rows;
+    plan->halves = plan->pair == 2 ? 2 : 1;
+    // split pairs own twice the work per unit of time: twice longer segments
+    // keep the same balance with half the partial traffic
+    plan->seg_len = (seg_rows > 0 ? seg_rows : plan->pair == 2 ? 2 * kSketchSegRows : kSketchSegRows) / plan->kc_rows;
     plan->nseg = (plan->nchunk + plan->seg_len - 1) / plan->seg_len;
-    plan->total_units = batch * (plan->ntiles_col / P) * plan->nseg;
+    plan->total_units = batch * (plan->ntiles_col / TP) * plan->nseg;
     int64_t owners = plan->pair ? std::min<int64_t>(pairs, num_sms / 2) : num_sms;
     if (owners > plan->total_units) owners = plan->total_units;
     plan->grid = static_cast<int>(owners * P);
     plan->smem = 0;
     plan->partial_elems =
-        static_cast<size_t>(batch) * plan->ntiles_col * plan->nseg * plan->ell_pad * plan->nt;
+        static_cast<size_t>(batch) * plan->ntiles_col * plan->nseg * plan->halves * plan->ell_pad * plan->nt;
     return true;
 }
 
 cudaError_t launch_sketch_tc(const SketchParams& p, const SketchPlan& plan, const CUtensorMap* tmap,
                              cudaStream_t stream) {
     if (p.omega_mode != 1) return cudaErrorInvalidValue;
-    if (plan.pair) {
+    if (plan.pair == 2) return plan.ell_pad == 80 ? launch_t<80, 2>(p, plan, tmap, stream) : cudaErrorInvalidValue;
+    if (plan.pair == 1) {
         switch (plan.ell_pad) {
-            case 16: return launch_t<16, true>(p, plan, tmap, stream);
-            case 32: return launch_t<32, true>(p, plan, tmap, stream);
-            case 48: return launch_t<48, true>(p, plan, tmap, stream);
-            case 64: return launch_t<64, true>(p, plan, tmap, stream);
+            case 16: return launch_t<16, 1>(p, plan, tmap, stream);
+            case 32: return launch_t<32, 1>(p, plan, tmap, stream);
+            case 48: return launch_t<48, 1>(p, plan, tmap, stream);
+            case 64: return launch_t<64, 1>(p, plan, tmap, stream);
             default: return cudaErrorInvalidValue;
         }
     }
     switch (plan.ell_pad) {
-        case 16: return launch_t<16, false>(p, plan, tmap, stream);
-        case 32: return launch_t<32, false>(p, plan, tmap, stream);
-        case 48: return launch_t<48, false>(p, plan, tmap, stream);
-        case 64: return launch_t<64, false>(p, plan, tmap, stream);
+        case 16: return launch_t<16, 0>(p, plan, tmap, stream);
+        case 32: return launch_t<32, 0>(p, plan, tmap, stream);
+        case 48: return launch_t<48, 0>(p, plan, tmap, stream);
+        case 64: return launch_t<64, 0>(p, plan, tmap, stream);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -11,7 +11,8 @@ of A is rounded once, to the fixed point of its epoch -- a multiple of
 everything after that is exact integer arithmetic until one fp64 conversion
 per epoch and a fixed-order fp64 sum of the segment partials. So per entry
     |Y - Y_exact|(i,j) <= 2^-47 sum_k |Omega(i,k)| M_j(k) + (nseg + 2) u (|Omega||A|)(i,j)
-with M_j(k) the largest |A(., j)| in row k's segment, u = 2^-53 (tested on
+with M_j(k) the largest |A(., j)| in row k's segment (4096 rows; 8192 with
+two partials per segment for the single-pass ell in (64, 80]), u = 2^-53 (tested on
 every case below against the product in extended precision, np.longdouble).
 The reference sketch is the sequential fp64 matmul
 (proj/src/dense_matrix.cpp:38-53), whose own per-entry bound is
@@ -65,19 +66,27 @@ def kernel(request, engine):
     _pairs(engine, 1)
 
 
-SEG_ROWS = 4096
+def _segments(ell):
+    """(rows per segment, partials per segment) of the passes sketching ell
+    rows (api.cu do_sketch: one pass up to 80 rows, else even passes of whole
+    16-row groups): 4096 and 1, or for passes of 65-80 rows, run by the
+    slice-split CTA pair, 8192 and 2 (csrc/sketch_tc.cu)."""
+    passes = -(-ell // 80)
+    width = ell if passes == 1 else min(80, 16 * -(-(-(-ell // passes)) // 16))
+    return (8192, 2) if width > 64 else (4096, 1)
 
 
 def _contract(om, a):
     """The per-entry bound of the fixed-point sketch (see the module doc)."""
     m = a.shape[0]
-    nseg = -(-m // SEG_ROWS)
+    seg_rows, halves = _segments(om.shape[0])
+    nseg = -(-m // seg_rows)
     M = np.empty_like(a)
     for g in range(nseg):
-        blk = np.abs(a[g * SEG_ROWS:(g + 1) * SEG_ROWS])
-        M[g * SEG_ROWS:(g + 1) * SEG_ROWS] = blk.max(axis=0, keepdims=True)
+        blk = np.abs(a[g * seg_rows:(g + 1) * seg_rows])
+        M[g * seg_rows:(g + 1) * seg_rows] = blk.max(axis=0, keepdims=True)
     B = np.abs(om) @ np.abs(a)
-    return (2.0 ** -47 * (np.abs(om) @ M) + (nseg + 2) * U * B) * (1 + 1e-9), B
+    return (2.0 ** -47 * (np.abs(om) @ M) + (halves * nseg + 2) * U * B) * (1 + 1e-9), B
 
 
 def _bound_check(y, om, a, exact=True, gamma=False):
@@ -156,7 +165,8 @@ def test_sketch_matches_dmma_kernel(engine, spid):
         assert np.all(d <= cb + 2 * _gamma(20000) * B)
 
 
-def test_exponent_changes_and_zero_columns(engine, spid):
+@pytest.mark.parametrize("ell", [48, 80])
+def test_exponent_changes_and_zero_columns(engine, spid, ell):
     """Columns whose magnitude grows far beyond the first rows' exponent (the
     headroom slow path), all-zero columns, columns zero then nonzero, and
     extreme but finite magnitudes."""
@@ -171,11 +181,12 @@ def test_exponent_changes_and_zero_columns(engine, spid):
     A[0, 5, 12345] = 1e6                       # one spike far above the rest
     A[1, 6] = torch.where(r % 2 == 0, 1e-8, 1e4)  # alternating scales
     A[1, 7, ::1000] *= 1e10
-    Y, _ = _check(engine, spid, A, 48, seed=3, base=0)
+    Y, _ = _check(engine, spid, A, ell, seed=3, base=0)
     assert torch.equal(Y[0, 1], torch.zeros_like(Y[0, 1]))
 
 
-def test_adversarial_fixed_point_columns(engine, spid):
+@pytest.mark.parametrize("ell", [48, 80])
+def test_adversarial_fixed_point_columns(engine, spid, ell):
     """Columns built against the per-epoch fixed point: an O(1) spike in a
     segment's first stage followed by a long 1e-12 tail in the same segment
     (the tail would be quantised at the spike's scale without the fallback),
@@ -193,7 +204,7 @@ def test_adversarial_fixed_point_columns(engine, spid):
     A[0, 4, 16:] *= 2.0 ** -30
     A[0, 5, ::2] = 0.0                         # half zeros
     A[0, 6] = torch.where(torch.arange(m, device="cuda") % 64 < 32, 1.0, 1e-15).double() * A[0, 6]
-    _check(engine, spid, A, 48, seed=17, base=2)
+    _check(engine, spid, A, ell, seed=17, base=2)
 
 
 def test_nonfinite_poisons_column(engine):
