@@ -123,7 +123,16 @@ int spidgpu_debug_counters(spidgpu_handle h, int64_t* out, int n, int reset);
  * reference sketch entry subsample()/subsample_column() (proj/src/grid.cpp:
  * 136-150, used by spid() at proj/src/id.cpp:75-80) with the Gaussian sketch
  * of the north star; restated by matmul (proj/src/dense_matrix.cpp:38-53).
- * FP64 DMMA, A staged by TMA, deterministic split-K. */
+ * Philox Omega (SPIDGPU_OMEGA_PHILOX, the performance mode): an exact
+ * integer-sliced contraction on the tcgen05 tensor cores (kind::i8, TMEM
+ * accumulators), A staged by TMA and read once (up to 80 rows per pass;
+ * 65-80 rows as slice-split CTA pairs). Explicit fp64 Omega (oracle mode):
+ * FP64 DMMA. Both split the work at fixed 4096-row segments (8192 for the
+ * split pairs) and sum the segment partials in a fixed order: Y is bitwise
+ * reproducible and independent of the batch it is computed in. Accuracy:
+ * per entry within 2^-47 sum_k |Omega(i,k)| M_j(k) + (2 nseg + 2) u (|Omega||A|)(i,j)
+ * of the exact product, M_j(k) the largest |A(., j)| of row k's segment
+ * (tests/test_gpu_sketch_i8.py). */
 int spidgpu_sketch_batched(spidgpu_handle h, const double* A, int64_t m, int64_t n, int64_t lda,
                            int64_t strideA, int64_t batch, int64_t ell, const spidgpu_omega* omega,
                            double* Y, int64_t ldy, int64_t strideY, void* stream);
@@ -162,11 +171,29 @@ int spidgpu_gather_batched(spidgpu_handle h, const double* A, int64_t m, int64_t
                            void* stream);
 
 /* B_s = A_s(J, :) for a strictly increasing row set J (nrows entries):
- * subsample (proj/src/grid.cpp:136-140). Output ld ldb, stride strideB. */
+ * subsample (proj/src/grid.cpp:136-140). Output ld ldb, stride strideB.
+ * Both batched gathers are asynchronous: an index outside the matrix
+ * (select_columns' IndexOutOfRange, proj/src/dense_matrix.cpp:75) leaves
+ * its column unwritten (rows: 0.0) and is recorded for
+ * spidgpu_stream_status. */
 int spidgpu_row_gather_batched(spidgpu_handle h, const double* A, int64_t m, int64_t n,
                                int64_t lda, int64_t strideA, int64_t batch, const int64_t* rows,
                                int64_t nrows, double* B, int64_t ldb, int64_t strideB,
                                void* stream);
+
+/* Workspaces. A handle's batched calls share one device workspace, like
+ * the reference's functions share nothing but their arguments per thread:
+ * issue them on ONE stream at a time (one handle per concurrent stream or
+ * host thread). Workspaces grow on first use (a cudaMalloc after
+ * synchronising the stream); spidgpu_reserve pre-sizes them for batches of
+ * up to `batch` m x n subdomains, sketches of up to ell rows and ranks up to
+ * kcap, so that later batched calls of those sizes allocate nothing. */
+int spidgpu_reserve(spidgpu_handle h, int64_t m, int64_t n, int64_t batch, int64_t ell, int64_t kcap);
+
+/* Synchronise `stream` and return the first deferred error a batched call
+ * of this handle recorded since the last call (IndexOutOfRange from the
+ * gathers), or SPID_OK; clears it. */
+int spidgpu_stream_status(spidgpu_handle h, void* stream);
 
 /* Exact verification terms per subdomain: err2[s] = ||A_s - skel_s C_s||_F^2,
  * ref2[s] = ||A_s||_F^2 (reconstruct + rel_frob_error, proj/src/id.cpp:85-90,
@@ -226,12 +253,12 @@ int spidgpu_spid(spidgpu_handle h, const double* a, int64_t m, int64_t n,
  * fine (m x k, m = P*nqoi) = M * coarse (|J| x k). Bit-identical to the
  * reference operator built by InterpOperator::from_spec. */
 int spidgpu_interp_apply(spidgpu_handle h, const spidgpu_grid_spec* spec, const double* coarse,
-                         int64_t k, double* fine);
+                         int64_t coarse_rows, int64_t k, double* fine);
 
 /* spid::reconstruct(SpidFactors) (proj/src/id.cpp:92-96): M * skel_c * C. */
 int spidgpu_spid_reconstruct(spidgpu_handle h, const spidgpu_grid_spec* spec,
-                             const double* coarse_skeleton, int64_t k, const double* coeffs,
-                             int64_t n, double* out);
+                             const double* coarse_skeleton, int64_t coarse_rows, int64_t k,
+                             const double* coeffs, int64_t coeff_rows, int64_t n, double* out);
 
 /* Batched device forms. gather: skel_c_s(:, t) = A_s(J, I_s[t]);
  * lift: fine_s(:, t) = M * coarse_s(:, t) for t < rank[s]. */
@@ -312,7 +339,7 @@ int spidgpu_crc32(spidgpu_handle h, const void* data, int64_t nbytes, int32_t on
 #define SPIDGPU_ARCHIVE_EXACT 0  /* column ID of each block's coarse rows: the
                                     reference's spid() -> byte-identical archive */
 #define SPIDGPU_ARCHIVE_SKETCH 1 /* Gaussian sketch (Philox) of the coarse rows
-                                    first, then the column ID (FP64 tensor cores) */
+                                    first (integer tcgen05 sketch), then the column ID */
 typedef struct spidgpu_archive_spec {
     int32_t naxes;              /* structured grid, 1..3 axes (axis 0 fastest)  */
     int32_t mode;               /* SPIDGPU_ARCHIVE_*                            */

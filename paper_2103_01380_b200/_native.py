@@ -120,6 +120,8 @@ _SIGS = {
     "spidgpu_abi_version": (C.c_int, []),
     "spidgpu_launch_count": (C.c_int64, [_H]),
     "spidgpu_set_option": (C.c_int, [_H, C.c_int, C.c_int64]),
+    "spidgpu_stream_status": (C.c_int, [_H, _vp]),
+    "spidgpu_reserve": (C.c_int, [_H, _i64, _i64, _i64, _i64, _i64]),
     "spidgpu_debug_counters": (C.c_int, [_H, C.POINTER(C.c_int64), C.c_int, C.c_int]),
     "spidgpu_sketch_batched": (C.c_int, [_H, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _OM, _vp,
                                          _i64, _i64, _vp]),
@@ -164,8 +166,8 @@ _SIGS = {
                                          _i64, _vp]),
     "spidgpu_row_indices": (C.c_int, [_GS, _vp, _i64, C.POINTER(C.c_int64)]),
     "spidgpu_spid": (C.c_int, [_H, _vp, _i64, _i64, _GS, _RR, _i64, _vp, _vp, _vp, _vp, _vp]),
-    "spidgpu_interp_apply": (C.c_int, [_H, _GS, _vp, _i64, _vp]),
-    "spidgpu_spid_reconstruct": (C.c_int, [_H, _GS, _vp, _i64, _vp, _i64, _vp]),
+    "spidgpu_interp_apply": (C.c_int, [_H, _GS, _vp, _i64, _i64, _vp]),
+    "spidgpu_spid_reconstruct": (C.c_int, [_H, _GS, _vp, _i64, _i64, _vp, _i64, _i64, _vp]),
     "spidgpu_gather_coarse_batched": (C.c_int, [_H, _vp, _i64, _i64, _i64, _i64, _i64, _GS, _vp,
                                                 _i64, _vp, _vp, _i64, _i64, _vp]),
     "spidgpu_interp_apply_batched": (C.c_int, [_H, _GS, _vp, _i64, _i64, _i64, _vp, _i64, _vp,

@@ -240,8 +240,10 @@ int do_gather(spidgpu_handle h, const double* A, int64_t m, int64_t n, int64_t l
     if (!A || !indices || !rank || !skel) return fail(h, SPID_INVALID_ARGUMENT, "null pointer");
     if (m < 1 || n < 1 || batch < 1 || kcap < 1) return fail(h, SPID_EMPTY_SELECTION, "empty gather");
     if (lda < m || ldskel < m) return fail(h, SPID_INVALID_ARGUMENT, "leading dimension too small");
+    // out-of-range indices (select_columns' IndexOutOfRange, dense_matrix.cpp:75)
+    // leave their columns unwritten and are reported through the deferred status
     CK(h, launch_gather_cols(A, m, lda, strideA, batch, indices, kcap, rank, n, skel, ldskel,
-                             strideS, nullptr, st));
+                             strideS, h->dev_status, st));
     h->launches += 1;
     return SPID_OK;
 }
@@ -550,6 +552,11 @@ int spidgpu_create(int device, spidgpu_handle* out) {
         return SPID_CUDA_ERROR;
     }
     h->encode = reinterpret_cast<EncodeTiledFn>(fn);
+    if (cudaMalloc(&h->dev_status, sizeof(int32_t)) != cudaSuccess ||
+        cudaMemset(h->dev_status, 0, sizeof(int32_t)) != cudaSuccess) {
+        delete h;
+        return SPID_CUDA_ERROR;
+    }
     for (int i = 0; i < 2; ++i) {
         if (cudaStreamCreateWithFlags(&h->lanes[i], cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&h->ev[i], cudaEventDisableTiming) != cudaSuccess) {
@@ -566,6 +573,7 @@ int spidgpu_destroy(spidgpu_handle h) {
     cudaSetDevice(h->device);
     cudaDeviceSynchronize();
     for (auto& w : h->ws) w.release();
+    if (h->dev_status) cudaFree(h->dev_status);
     if (h->archive_pinned) cudaFreeHost(h->archive_pinned);
     if (h->upload_pinned) cudaFreeHost(h->upload_pinned);
     for (cudaEvent_t e : h->upload_ev)
@@ -654,9 +662,44 @@ int spidgpu_row_gather_batched(spidgpu_handle h, const double* A, int64_t m, int
     if (nrows < 1) return fail(h, SPID_EMPTY_SKETCH, "row selection is empty");
     if (!A || !rows || !B || ldb < nrows || lda < m)
         return fail(h, SPID_INVALID_ARGUMENT, "bad row gather arguments");
-    CK(h, launch_gather_rows(A, m, n, lda, strideA, batch, rows, nrows, B, ldb, strideB,
+    CK(h, launch_gather_rows(A, m, n, lda, strideA, batch, rows, nrows, B, ldb, strideB, h->dev_status,
                              static_cast<cudaStream_t>(stream)));
     h->launches += 1;
+    return SPID_OK;
+}
+
+int spidgpu_reserve(spidgpu_handle h, int64_t m, int64_t n, int64_t batch, int64_t ell, int64_t kcap) {
+    if (!h || m < 1 || n < 1 || batch < 1 || ell < 1 || kcap < 1) return SPID_INVALID_ARGUMENT;
+    cudaSetDevice(h->device);
+    Workspace& ws = h->ws[0];
+    cudaStream_t st = nullptr;
+    const int sms = h->sketch_sms > 0 ? h->sketch_sms : h->num_sms;
+    size_t part = 0;
+    for (int64_t w : {std::min<int64_t>(ell, kSketchTcMaxEll), std::min<int64_t>(ell, 64), std::min<int64_t>(ell, 48)}) {
+        SketchPlan plan;
+        if (sketch_tc_make_plan(m, n, batch, w, sms, h->sketch_pairs, h->sketch_seg_rows, &plan))
+            part = std::max(part, plan.partial_elems);
+        if (sketch_make_plan(m, n, batch, std::min<int64_t>(w, 80), sms, &plan))
+            part = std::max(part, plan.partial_elems);
+    }
+    CK(h, ws.partial.ensure(part * sizeof(double), st));
+    CK(h, ws.rws.ensure(sizeof(double) * batch * kcap * n, st));
+    VerifyPlan vp;
+    if (kcap <= 80 && verify_make_plan(m, n, batch, kcap, h->num_sms, &vp))
+        CK(h, ws.vpart.ensure(sizeof(double) * vp.part_elems, st));
+    CK(h, cudaDeviceSynchronize());
+    return SPID_OK;
+}
+
+int spidgpu_stream_status(spidgpu_handle h, void* stream) {
+    if (!h) return SPID_INVALID_ARGUMENT;
+    cudaSetDevice(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int32_t v = 0;
+    CK(h, cudaMemcpyAsync(&v, h->dev_status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(h, cudaMemsetAsync(h->dev_status, 0, sizeof(int32_t), st));
+    CK(h, cudaStreamSynchronize(st));
+    if (v) return fail(h, v, "a batched gather on this stream met an index outside the matrix");
     return SPID_OK;
 }
 
@@ -774,7 +817,7 @@ int spidgpu_sub_id(spidgpu_handle h, const double* a, int64_t m, int64_t n, cons
     if (rc) return rc;
     CK(h, ws.ybuf.ensure(sizeof(double) * nrows * n, st));
     CK(h, launch_gather_rows(ws.a.as<double>(), m, n, lda, lda * n, 1, ws.rows.as<int64_t>(), nrows,
-                             ws.ybuf.as<double>(), nrows, nrows * n, st));
+                             ws.ybuf.as<double>(), nrows, nrows * n, nullptr, st));
     h->launches += 1;
     const int64_t kc = std::max<int64_t>(kcap, 1);
     CK(h, ws.idx.ensure(sizeof(int64_t) * kc, st));
@@ -1075,7 +1118,7 @@ int spidgpu_spid(spidgpu_handle h, const double* a, int64_t m, int64_t n,
     if (rc) return rc;
     CK(h, ws.ybuf.ensure(sizeof(double) * nrows * n, st));
     CK(h, launch_gather_rows(ws.a.as<double>(), m, n, lda, lda * n, 1, ws.rows.as<int64_t>(), nrows,
-                             ws.ybuf.as<double>(), nrows, nrows * n, st));  // subsample, grid.cpp:142-150
+                             ws.ybuf.as<double>(), nrows, nrows * n, nullptr, st));  // subsample, grid.cpp:142-150
     h->launches += 1;
     const int64_t kc = std::max<int64_t>(kcap, 1);
     CK(h, ws.idx.ensure(sizeof(int64_t) * kc, st));
@@ -1094,13 +1137,15 @@ int spidgpu_spid(spidgpu_handle h, const double* a, int64_t m, int64_t n,
 }
 
 int spidgpu_interp_apply(spidgpu_handle h, const spidgpu_grid_spec* spec, const double* coarse,
-                         int64_t k, double* fine) {
+                         int64_t coarse_rows, int64_t k, double* fine) {
     if (!h) return SPID_INVALID_ARGUMENT;
     if (!coarse || !fine || k < 1) return fail(h, SPID_INVALID_ARGUMENT, "null buffer / k < 1");
     GridSpecDev g;
     int64_t P = 0, Pc = 0;
     int rc = spec_to_dev(h, spec, &g, &P, &Pc);
     if (rc) return rc;
+    if (coarse_rows != Pc * g.nqoi)  // interp.cpp:170
+        return fail(h, SPID_DIMENSION_MISMATCH, "coarse rows != coarse points x nqoi");
     cudaSetDevice(h->device);
     Workspace& ws = h->ws[0];
     cudaStream_t st = h->lanes[0];
@@ -1118,22 +1163,26 @@ int spidgpu_interp_apply(spidgpu_handle h, const spidgpu_grid_spec* spec, const 
     CK(h, cudaMemcpyAsync(fine, ws.out.ptr, sizeof(double) * m * k, cudaMemcpyDeviceToHost, st));
     CK(h, cudaStreamSynchronize(st));
     if (flag)  // interp.cpp:27-29
-        return fail(h, SPID_GEOMETRY_MISMATCH,
-                    "ExtrapolationRequired: fine point beyond the last coarse point on a non-periodic axis");
+        return fail(h, SPID_EXTRAPOLATION_REQUIRED,
+                    "fine point beyond the last coarse point on a non-periodic axis");
     return SPID_OK;
 }
 
 int spidgpu_spid_reconstruct(spidgpu_handle h, const spidgpu_grid_spec* spec,
-                             const double* coarse_skeleton, int64_t k, const double* coeffs,
-                             int64_t n, double* out) {
+                             const double* coarse_skeleton, int64_t coarse_rows, int64_t k,
+                             const double* coeffs, int64_t coeff_rows, int64_t n, double* out) {
     if (!h) return SPID_INVALID_ARGUMENT;
     if (!coarse_skeleton || !coeffs || !out || k < 1 || n < 1)
         return fail(h, SPID_INVALID_ARGUMENT, "bad reconstruct arguments");
+    if (coeff_rows != k)  // id.cpp:93-94
+        return fail(h, SPID_DIMENSION_MISMATCH, "inconsistent factor dimensions");
     if (k > 80) return fail(h, SPID_SHAPE_UNSUPPORTED, "reconstruct supports rank <= 80");
     GridSpecDev g;
     int64_t P = 0, Pc = 0;
     int rc = spec_to_dev(h, spec, &g, &P, &Pc);
     if (rc) return rc;
+    if (coarse_rows != Pc * g.nqoi)  // interp.cpp:179 via id.cpp:95
+        return fail(h, SPID_DIMENSION_MISMATCH, "coarse skeleton rows != coarse points x nqoi");
     cudaSetDevice(h->device);
     Workspace& ws = h->ws[0];
     cudaStream_t st = h->lanes[0];
@@ -1158,7 +1207,7 @@ int spidgpu_spid_reconstruct(spidgpu_handle h, const spidgpu_grid_spec* spec,
     CK(h, cudaMemcpyAsync(&flag, ws.flag.ptr, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(h, cudaMemcpyAsync(out, ws.out.ptr, sizeof(double) * m * n, cudaMemcpyDeviceToHost, st));
     CK(h, cudaStreamSynchronize(st));
-    if (flag) return fail(h, SPID_GEOMETRY_MISMATCH, "ExtrapolationRequired");
+    if (flag) return fail(h, SPID_EXTRAPOLATION_REQUIRED, "fine point beyond the last coarse point");
     return SPID_OK;
 }
 

@@ -237,8 +237,10 @@ int parse_block(const uint8_t* bytes, const SecRef& s, BlockRef* b, std::string*
         if (!r.need(16)) return trunc("archive ends before the promised payload");
         const uint64_t rows = r.u64(), cols = r.u64();
         if (rows == 0 || cols == 0) return trunc("matrix section has empty dimensions");
-        if (rows > static_cast<uint64_t>(r.size) || cols > static_cast<uint64_t>(r.size) ||
-            rows * cols > static_cast<uint64_t>((r.size - r.at) / 8))
+        // division, not rows * cols: the product of two section-sized
+        // values can wrap uint64 and pass a multiplied check
+        const uint64_t avail = static_cast<uint64_t>((r.size - r.at) / 8);
+        if (rows > avail || cols > avail || cols > avail / rows)
             return trunc("archive ends before the promised payload");
         dims[mat][0] = static_cast<int64_t>(rows);
         dims[mat][1] = static_cast<int64_t>(cols);

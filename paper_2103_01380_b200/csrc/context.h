@@ -91,6 +91,9 @@ struct spidgpu_context {
     uint8_t* upload_pinned = nullptr;
     size_t upload_cap = 0;
     cudaEvent_t upload_ev[16] = {};
+    // deferred status of asynchronous batched calls (first error wins; read
+    // and cleared by spidgpu_stream_status): out-of-range gather indices
+    int32_t* dev_status = nullptr;
 };
 
 namespace spidgpu {

@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(kThreads)
         if (t >= rank[s]) continue;
         const int64_t col = idx[s * kcap + t];
         if (col < 0 || col >= n) {  // dense_matrix.cpp:75 (IndexOutOfRange)
-            if (err_flag && threadIdx.x == 0) atomicExch(err_flag, SPID_INDEX_OUT_OF_RANGE);
+            if (err_flag && threadIdx.x == 0) atomicCAS(err_flag, 0, SPID_INDEX_OUT_OF_RANGE);
             continue;
         }
         const double* src = A + s * strideA + col * lda;
@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void gather_rows_kernel(const double* __restrict__ A, int64_t m, int64_t n,
                                    int64_t lda, int64_t strideA, int64_t batch,
                                    const int64_t* __restrict__ rows, int64_t nrows,
-                                   double* __restrict__ B, int64_t ldb, int64_t strideB) {
+                                   double* __restrict__ B, int64_t ldb, int64_t strideB, int32_t* err_flag) {
     const int64_t total = batch * n * nrows;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -62,7 +62,9 @@ __global__ void gather_rows_kernel(const double* __restrict__ A, int64_t m, int6
         const int64_t j = (e / nrows) % n;
         const int64_t s = e / (nrows * n);
         const int64_t r = rows[i];
-        B[s * strideB + j * ldb + i] = (r >= 0 && r < m) ? A[s * strideA + j * lda + r] : 0.0;
+        const bool ok = r >= 0 && r < m;  // grid.cpp:138-140 (rows beyond the matrix)
+        if (!ok && err_flag) atomicCAS(err_flag, 0, SPID_INDEX_OUT_OF_RANGE);
+        B[s * strideB + j * ldb + i] = ok ? A[s * strideA + j * lda + r] : 0.0;
     }
 }
 
@@ -90,7 +92,7 @@ cudaError_t launch_gather_cols(const double* A, int64_t m, int64_t lda, int64_t 
 
 cudaError_t launch_gather_rows(const double* A, int64_t m, int64_t n, int64_t lda,
                                int64_t strideA, int64_t batch, const int64_t* rows,
-                               int64_t nrows, double* B, int64_t ldb, int64_t strideB,
+                               int64_t nrows, double* B, int64_t ldb, int64_t strideB, int32_t* err_flag,
                                cudaStream_t stream) {
     const int64_t total = batch * n * nrows;
     int64_t grid = (total + 255) / 256;
@@ -98,7 +100,7 @@ cudaError_t launch_gather_rows(const double* A, int64_t m, int64_t n, int64_t ld
     if (grid < 1) grid = 1;
     gather_rows_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(A, m, n, lda, strideA,
                                                                         batch, rows, nrows, B,
-                                                                        ldb, strideB);
+                                                                        ldb, strideB, err_flag);
     return cudaGetLastError();
 }
 

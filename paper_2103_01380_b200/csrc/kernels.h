@@ -121,7 +121,7 @@ cudaError_t launch_gather_cols(const double* A, int64_t m, int64_t lda, int64_t 
                                int64_t strideS, int32_t* err_flag, cudaStream_t stream);
 cudaError_t launch_gather_rows(const double* A, int64_t m, int64_t n, int64_t lda,
                                int64_t strideA, int64_t batch, const int64_t* rows,
-                               int64_t nrows, double* B, int64_t ldb, int64_t strideB,
+                               int64_t nrows, double* B, int64_t ldb, int64_t strideB, int32_t* err_flag,
                                cudaStream_t stream);
 
 // ---- verify / reconstruct (verify.cu) ------------------------------------

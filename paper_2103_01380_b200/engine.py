@@ -62,7 +62,11 @@ class CompressResult:
 
 
 class Engine:
-    """spidgpu handle bound to one device, with torch-allocated buffers."""
+    """spidgpu handle bound to one device, with torch-allocated buffers.
+
+    One Engine's calls share the handle's device workspace: issue them on one
+    stream at a time (use one Engine per concurrent stream), see
+    include/spidgpu.h "Workspaces"."""
 
     def __init__(self, device: int = 0):
         self.device = device
@@ -71,6 +75,16 @@ class Engine:
 
     def launches(self) -> int:
         return self.h.launches()
+
+    def reserve(self, m: int, n: int, batch: int, ell: int, kcap: int) -> None:
+        """Pre-size the workspaces (spidgpu_reserve): later calls of these
+        sizes allocate nothing."""
+        self.h.check(N.lib.spidgpu_reserve(self.h.h, m, n, batch, ell, kcap))
+
+    def stream_status(self, stream=None) -> None:
+        """Synchronise and raise the first deferred error of batched calls
+        (out-of-range gather indices) -- spidgpu_stream_status."""
+        self.h.check(N.lib.spidgpu_stream_status(self.h.h, _stream(stream)))
 
     # ---- inputs -----------------------------------------------------------------
     def alloc_field(self, cfg: SpidConfig, batch: int) -> torch.Tensor:

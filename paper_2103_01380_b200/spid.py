@@ -333,7 +333,7 @@ def interp_apply(dims, strides, coarse, periodic=None, *, include_boundary=True,
     P = int(np.prod(dims)) * nqoi
     fine = np.zeros((P, c.shape[1]), order="F")
     h = _h(device)
-    h.check(N.lib.spidgpu_interp_apply(h.h, C.byref(spec), _ptr(c), c.shape[1], _ptr(fine)))
+    h.check(N.lib.spidgpu_interp_apply(h.h, C.byref(spec), _ptr(c), c.shape[0], c.shape[1], _ptr(fine)))
     return fine
 
 
@@ -347,8 +347,8 @@ def spid_reconstruct(factors: SpidFactors, *, device=0):
     m *= int(factors.spec.nqoi)
     out = np.zeros((m, c.shape[1]), order="F")
     h = _h(device)
-    h.check(N.lib.spidgpu_spid_reconstruct(h.h, C.byref(factors.spec), _ptr(s), s.shape[1],
-                                           _ptr(c), c.shape[1], _ptr(out)))
+    h.check(N.lib.spidgpu_spid_reconstruct(h.h, C.byref(factors.spec), _ptr(s), s.shape[0], s.shape[1],
+                                           _ptr(c), c.shape[0], c.shape[1], _ptr(out)))
     return out
 
 

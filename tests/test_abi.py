@@ -68,16 +68,24 @@ def test_null_handle_rejected():
     assert N.lib.spidgpu_last_error(None) == b""
 
 
-def test_sass_is_sm100a_with_dmma_and_tma():
-    """The sketch object holds sm_100a SASS with DMMA (FP64 tensor cores) and
-    UTMALDG (TMA) -- checked with cuobjdump, no GPU needed."""
-    obj = os.path.join(ROOT, "paper_2103_01380_b200", "lib", "obj", "sketch.o")
-    if not os.path.exists(obj):
+@pytest.mark.parametrize("obj,mnemonics", [
+    # the shipped Philox sketch: tcgen05 integer MMAs, TMEM loads/stores, TMA,
+    # multicast MMA commits (CTA pairs) and st.async (DSMEM) of the split pair
+    ("sketch_tc.o", ["UTCIMMA", "LDTM", "STTM", "UTMALDG", "UTCBAR.MULTICAST", "STAS"]),
+    # the explicit-Omega (oracle-mode) sketch and the verify kernel: FP64 tensor cores + TMA
+    ("sketch.o", ["DMMA.8x8x4", "UTMALDG"]),
+    ("verify_tma.o", ["DMMA.8x8x4", "UTMALDG"]),
+])
+def test_sass_is_sm100a_with_tensor_cores_and_tma(obj, mnemonics):
+    """The kernel objects hold sm_100a SASS with the instructions their design
+    relies on -- checked with cuobjdump, no GPU needed."""
+    path = os.path.join(ROOT, "paper_2103_01380_b200", "lib", "obj", obj)
+    if not os.path.exists(path):
         pytest.skip("objects not built")
-    out = subprocess.run(["cuobjdump", "-sass", obj], capture_output=True, text=True).stdout
+    out = subprocess.run(["cuobjdump", "-sass", path], capture_output=True, text=True).stdout
     assert "sm_100a" in out
-    assert "DMMA.8x8x4" in out
-    assert "UTMALDG" in out
+    for mn in mnemonics:
+        assert mn in out, mn
 
 
 def test_rank_rule_validation():

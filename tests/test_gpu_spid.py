@@ -101,3 +101,66 @@ def test_spid_errors(spid, orc):
     with pytest.raises(spid.SpidError) as e:
         spid.spid(a, [24], [5], rank=1, include_boundary=False)
     assert e.value.name == "ExtrapolationRequired"
+
+
+def test_lift_and_reconstruct_check_factor_shapes(spid, orc):
+    """interp_apply / spid_reconstruct take the coarse row count and the
+    coefficient row count through the C ABI and raise DimensionMismatch on
+    inconsistent factors (proj/src/interp.cpp:170,179; proj/src/id.cpp:93-94)
+    instead of reading past the host buffers; extrapolation is reported
+    under its own name (interp.cpp:27-29)."""
+    coarse = orc.seeded_matrix(7, 3, 2)  # 24 points, stride 4, boundary: 7 coarse points
+    spid.interp_apply([24], [4], coarse)
+    with pytest.raises(spid.SpidError) as e:
+        spid.interp_apply([24], [4], coarse[:6])
+    assert e.value.name == "DimensionMismatch"
+    with pytest.raises(spid.SpidError) as e:
+        spid.interp_apply([24], [5], orc.seeded_matrix(5, 3, 2), include_boundary=False)
+    assert e.value.name == "ExtrapolationRequired"
+    a = orc.seeded_matrix(24, 9, 1)
+    f = spid.spid(a, [24], [4], rank=2)
+    spid.spid_reconstruct(f["factors"])
+    base = f["factors"].base
+    good_c = base.coeffs
+    base.coeffs = good_c[:1]
+    with pytest.raises(spid.SpidError) as e:
+        spid.spid_reconstruct(f["factors"])
+    assert e.value.name == "DimensionMismatch"
+    base.coeffs, good_s = good_c, base.skeleton
+    base.skeleton = good_s[:5]
+    with pytest.raises(spid.SpidError) as e:
+        spid.spid_reconstruct(f["factors"])
+    assert e.value.name == "DimensionMismatch"
+    base.skeleton = good_s
+
+
+def test_batched_gather_reports_out_of_range_indices(engine):
+    """The asynchronous gathers record an index outside the matrix
+    (select_columns' IndexOutOfRange, proj/src/dense_matrix.cpp:75) for
+    spidgpu_stream_status; valid columns are still gathered."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2103_01380_b200 import _native as N
+
+    A = torch.randn((2, 10, 64), dtype=torch.float64, device="cuda")
+    idx = torch.tensor([[3, 9], [1, 10]], dtype=torch.int64, device="cuda")  # 10 is out of range
+    rank = torch.tensor([2, 2], dtype=torch.int64, device="cuda")
+    skel = torch.zeros((2, 2, 64), dtype=torch.float64, device="cuda")
+    p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    engine.h.check(N.lib.spidgpu_gather_batched(engine.h.h, p(A), 64, 10, 64, 640, 2, p(idx), 2, p(rank),
+                                                p(skel), 64, 128, None))
+    with pytest.raises(N.SpidError) as e:
+        engine.stream_status()
+    assert e.value.name == "IndexOutOfRange"
+    engine.stream_status()  # cleared
+    assert torch.equal(skel[0, 0], A[0, 3]) and torch.equal(skel[1, 0], A[1, 1])
+    rows = torch.tensor([0, 5, 64], dtype=torch.int64, device="cuda")
+    B = torch.empty((2, 10, 3), dtype=torch.float64, device="cuda")
+    engine.h.check(N.lib.spidgpu_row_gather_batched(engine.h.h, p(A), 64, 10, 64, 640, 2, p(rows), 3, p(B), 3,
+                                                    30, None))
+    with pytest.raises(N.SpidError) as e:
+        engine.stream_status()
+    assert e.value.name == "IndexOutOfRange"
+    engine.reserve(64, 10, 2, 48, 8)
