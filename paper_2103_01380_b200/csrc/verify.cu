@@ -216,30 +216,62 @@ cudaError_t launch_verify(const VerifyParams& p, int /*num_sms*/, cudaStream_t s
     return cudaGetLastError();
 }
 
+// out_s = skel_s * C_s exactly as the reference's matmul forms it
+// (proj/src/dense_matrix.cpp:38-53): c(i, j) = sum over t ascending of
+// skel(i, t) * C(t, j), each product and sum rounded separately (DMUL, DADD:
+// no FMA, no tensor-core accumulation), terms with C(t, j) == 0 skipped --
+// so reconstruct() is bit-identical to the reference, not just close. One
+// thread per output row, kRecCols columns per block, C's slab in shared
+// memory (the zero test is warp-uniform).
+constexpr int kRecRows = 128, kRecCols = 32;
+
+__global__ void __launch_bounds__(kRecRows) reconstruct_exact_kernel(
+    const double* __restrict__ skel, int64_t m, int64_t ldskel, int64_t strideS, const double* __restrict__ C,
+    int64_t kcap, int64_t strideC, const int64_t* __restrict__ rank, int64_t n, double* __restrict__ out,
+    int64_t ldo, int64_t strideO, int64_t rblocks, int64_t cblocks) {
+    extern __shared__ double cs[];  // [kRecCols][k]
+    const int64_t s = blockIdx.x / (rblocks * cblocks);
+    const int64_t rb = (blockIdx.x / cblocks) % rblocks, cb = blockIdx.x % cblocks;
+    const int k = static_cast<int>(rank[s]);
+    const int64_t j0 = cb * kRecCols;
+    const int nc = static_cast<int>(n - j0 < kRecCols ? n - j0 : kRecCols);
+    const double* Cs = C + s * strideC;
+    for (int e = threadIdx.x; e < nc * k; e += kRecRows) {
+        const int jj = e / k, t = e % k;
+        cs[jj * k + t] = Cs[(j0 + jj) * kcap + t];
+    }
+    __syncthreads();
+    const int64_t i = rb * kRecRows + threadIdx.x;
+    if (i >= m) return;
+    const double* S = skel + s * strideS + i;
+    double acc[kRecCols];
+#pragma unroll
+    for (int jj = 0; jj < kRecCols; ++jj) acc[jj] = 0.0;
+    for (int t = 0; t < k; ++t) {
+        const double a = S[t * ldskel];
+#pragma unroll
+        for (int jj = 0; jj < kRecCols; ++jj) {
+            if (jj < nc) {
+                const double b = cs[jj * k + t];
+                if (b != 0.0) acc[jj] = __dadd_rn(acc[jj], __dmul_rn(a, b));
+            }
+        }
+    }
+    double* o = out + s * strideO + i;
+#pragma unroll
+    for (int jj = 0; jj < kRecCols; ++jj)
+        if (jj < nc) o[(j0 + jj) * ldo] = acc[jj];
+}
+
 cudaError_t launch_reconstruct(const double* skel, int64_t m, int64_t ldskel, int64_t strideS,
                                const double* C, int64_t kcap, int64_t strideC,
                                const int64_t* rank, int64_t n, int64_t batch, double* out,
                                int64_t ldo, int64_t strideO, cudaStream_t stream) {
     if (kcap > kMaxK) return cudaErrorInvalidValue;
-    VerifyParams p{};
-    p.m = m;
-    p.n = n;
-    p.batch = batch;
-    p.skel = skel;
-    p.ldskel = ldskel;
-    p.strideS = strideS;
-    p.C = C;
-    p.kcap = kcap;
-    p.strideC = strideC;
-    p.rank = rank;
-    p.nblk = verify_row_blocks(m);
-    const size_t smem = slab_smem(kcap);
-    cudaError_t e = cudaFuncSetAttribute(slab_kernel<false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    slab_kernel<false><<<static_cast<unsigned>(batch * p.nblk), kThreads, smem, stream>>>(
-        p, out, ldo, strideO);
+    const int64_t rblocks = (m + kRecRows - 1) / kRecRows, cblocks = (n + kRecCols - 1) / kRecCols;
+    const size_t smem = sizeof(double) * kRecCols * kcap;
+    reconstruct_exact_kernel<<<static_cast<unsigned>(batch * rblocks * cblocks), kRecRows, smem, stream>>>(
+        skel, m, ldskel, strideS, C, kcap, strideC, rank, n, out, ldo, strideO, rblocks, cblocks);
     return cudaGetLastError();
 }
 

@@ -282,3 +282,18 @@ def test_both_cpqr_kernels_bitwise(spid, orc, m, n, k):
             assert _eq(q["q"], qo.q) and _eq(q["r"], qo.r) and _eq(q["pivots"], qo.pivots)
     finally:
         N.lib.spidgpu_set_option(h.h, N.SPIDGPU_OPT_GENERIC_CPQR, 0)
+
+
+@pytest.mark.parametrize("m,k,n", [(37, 5, 11), (300, 32, 70), (1000, 80, 40)])
+def test_reconstruct_bitwise_vs_reference_matmul(spid, orc, ref, m, k, n):
+    """reconstruct = the reference's matmul (proj/src/dense_matrix.cpp:38-53)
+    bit for bit: separately rounded products and sums in ascending k, zero
+    coefficients skipped (an identity block and sparse C included)."""
+    s = orc.seeded_matrix(m, k, 3 + m)
+    c = orc.seeded_matrix(k, n, 4 + n)
+    c[:, : min(k, n)] = np.eye(k)[:, : min(k, n)]
+    c[:, -1] = 0.0
+    c[k // 2] = 0.0
+    got = spid.reconstruct(s, np.asfortranarray(c))
+    assert np.array_equal(got, orc.matmul(s, np.asfortranarray(c)))
+    assert np.array_equal(got, ref.matmul(s, np.asfortranarray(c)))
