@@ -428,6 +428,34 @@ typedef struct spidgpu_stream_stats {
 
 typedef struct spidgpu_stream* spidgpu_stream_handle;
 
+/* The pipeline's event log (spid::TaskEvent, proj/include/spid/pipeline.hpp:
+ * 24-32). Times are seconds on the DEVICE timeline from the stream's open
+ * (CUDA events recorded on the ingestion and stage-1 streams), so causality
+ * is exact: a chunk's stage 1 waits on the event that closes it.
+ *   SNAPSHOT_INGESTED  per frame; chunk = snapshot index; duration = device
+ *                      time of the push that carried it (host copy + gather)
+ *   CHUNK_CLOSED       per (block, chunk): ingestion of the chunk complete
+ *   STAGE1_DONE        per (block, chunk); duration = the batched stage-1
+ *                      launch of that chunk (all blocks)
+ *   STAGE2_DONE        per block; duration = stage 2 + archive emission */
+#define SPIDGPU_EVENT_SNAPSHOT_INGESTED 0
+#define SPIDGPU_EVENT_CHUNK_CLOSED 1
+#define SPIDGPU_EVENT_STAGE1_DONE 2
+#define SPIDGPU_EVENT_STAGE2_DONE 3
+typedef struct spidgpu_task_event {
+    int32_t kind;
+    int64_t block;   /* -1 for stream-level events */
+    int64_t chunk;   /* snapshot index for SNAPSHOT_INGESTED */
+    double wall_time;
+    double duration;
+} spidgpu_task_event;
+
+typedef struct spidgpu_overlap {  /* spid::OverlapReport, pipeline.hpp:52-56 */
+    double overlap_fraction;      /* of stage-1 time inside ingestion activity */
+    double stage1_busy_seconds;
+    double producer_busy_seconds;
+} spidgpu_overlap;
+
 /* Validates the plan (UnstructuredNoInterp, BadStreamConfig, BlockTooSmall,
  * BadSubsampleSpec as run_pipeline does before ingesting). The stream owns
  * its CUDA streams and buffers; `h` receives the archive at finish. */
@@ -446,6 +474,13 @@ int spidgpu_stream_finish(spidgpu_stream_handle s, int64_t* nbytes);
 int spidgpu_stream_get_stats(spidgpu_stream_handle s, spidgpu_stream_stats* out);
 /* Message of the stream's last failure ("" if none). */
 const char* spidgpu_stream_last_error(spidgpu_stream_handle s);
+/* After spidgpu_stream_finish: the event log, in emission order per kind
+ * (ingestion, chunk closes, stage-1 completions, stage-2 completions).
+ * Writes min(cap, total) events; *count = total. */
+int spidgpu_stream_events(spidgpu_stream_handle s, spidgpu_task_event* out, int64_t cap, int64_t* count);
+/* spid::overlap_report (proj/src/pipeline.cpp:296-332): pure host arithmetic
+ * over an event log; EmptyLog for an empty one. */
+int spidgpu_overlap_report(const spidgpu_task_event* events, int64_t count, spidgpu_overlap* out);
 int spidgpu_stream_close(spidgpu_stream_handle s);
 
 /* =====================================================================

@@ -39,6 +39,7 @@ enum spidgpu_status {
     SPID_UNSTRUCTURED_NO_INTERP = 24,/* "UnstructuredNoInterp" archive.cpp:291; interp.cpp:47 */
     SPID_BAD_STREAM_CONFIG = 25,/* "BadStreamConfig"  pipeline.cpp:110-113; spid_cli.cpp:248-263 */
     SPID_SHORT_STREAM = 26,     /* "ShortStream"      pipeline.cpp:246-247 */
+    SPID_EMPTY_LOG = 27,        /* "EmptyLog"         pipeline.cpp:297 */
     /* codes that exist only on the device path */
     SPID_CUDA_ERROR = 100,      /* "CudaError" */
     SPID_INVALID_ARGUMENT = 101,/* "InvalidArgument" (null pointer, bad leading dim) */

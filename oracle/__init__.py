@@ -36,7 +36,7 @@ STATUS_NAMES = {
     10: "IndexOutOfRange", 11: "GeometryMismatch", 12: "ZeroReference",
     13: "ZeroDenominator", 14: "BadSubsampleSpec", 15: "EmptySketch", 16: "ExtrapolationRequired", 17: "BadGridGeom",
     18: "BlockTooSmall", 19: "BadMagic", 20: "VersionUnsupported", 21: "TruncatedPayload",
-    22: "ChecksumMismatch", 23: "CoverageGap", 24: "UnstructuredNoInterp", 25: "BadStreamConfig", 26: "ShortStream",
+    22: "ChecksumMismatch", 23: "CoverageGap", 24: "UnstructuredNoInterp", 25: "BadStreamConfig", 26: "ShortStream", 27: "EmptyLog",
     100: "CudaError", 101: "InvalidArgument", 102: "ShapeUnsupported", 103: "NoDevice",
 }
 

@@ -102,6 +102,18 @@ class StreamStats(C.Structure):
                 ("stage1_ms", C.c_double), ("stage2_ms", C.c_double)]
 
 
+class TaskEvent(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("block", C.c_int64), ("chunk", C.c_int64), ("wall_time", C.c_double),
+                ("duration", C.c_double)]
+
+
+class Overlap(C.Structure):
+    _fields_ = [("overlap_fraction", C.c_double), ("stage1_busy_seconds", C.c_double),
+                ("producer_busy_seconds", C.c_double)]
+
+
+EVENT_KINDS = ("SnapshotIngested", "ChunkClosed", "Stage1Done", "Stage2Done")
+
 _vp = C.c_void_p
 _i64 = C.c_int64
 _H = C.c_void_p
@@ -160,6 +172,8 @@ _SIGS = {
     "spidgpu_stream_push": (C.c_int, [_vp, _vp, _i64, _i64, _i64, C.c_int32]),
     "spidgpu_stream_finish": (C.c_int, [_vp, _pi64]),
     "spidgpu_stream_get_stats": (C.c_int, [_vp, C.POINTER(StreamStats)]),
+    "spidgpu_stream_events": (C.c_int, [_vp, C.POINTER(TaskEvent), _i64, C.POINTER(C.c_int64)]),
+    "spidgpu_overlap_report": (C.c_int, [C.POINTER(TaskEvent), _i64, C.POINTER(Overlap)]),
     "spidgpu_stream_last_error": (C.c_char_p, [_vp]),
     "spidgpu_stream_close": (C.c_int, [_vp]),
     "spidgpu_field_generate": (C.c_int, [_H, C.POINTER(FieldSpec), _i64, _i64, _vp, _vp, _i64,

@@ -91,6 +91,7 @@ bool omega_ok(const spidgpu_omega* om) {
 int do_sketch(spidgpu_handle h, Workspace& ws, const double* A, int64_t m, int64_t n, int64_t lda,
               int64_t strideA, int64_t batch, int64_t ell, const spidgpu_omega* om, double* Y,
               int64_t ldy, int64_t strideY, cudaStream_t st) {
+    NvtxRange nvtx_range("spidgpu.sketch");
     if (m < 1 || n < 1 || batch < 1 || ell < 1) return fail(h, SPID_EMPTY_MATRIX, "empty sketch shape");
     if (!A || !Y || !omega_ok(om)) return fail(h, SPID_INVALID_ARGUMENT, "null pointer / omega");
     if (lda < m || ldy < ell || strideA < lda * n || strideY < ldy * (n - 1) + ell)
@@ -164,6 +165,7 @@ int do_cpqr(spidgpu_handle h, Workspace& ws, const double* Y, int64_t rows, int6
             int64_t strideY, int64_t batch, const spidgpu_rank_rule* rule, int64_t kcap,
             int64_t* indices, double* C, int64_t strideC, int64_t* rank, double* resid,
             int32_t* status, int64_t* pivots, double* R, double* Q, cudaStream_t st) {
+    NvtxRange nvtx_range("spidgpu.cpqr");
     if (rows < 1 || n < 1 || batch < 1) return fail(h, SPID_EMPTY_MATRIX, "empty matrix");
     if (!Y || !indices || !C || !rank || !resid || !status)
         return fail(h, SPID_INVALID_ARGUMENT, "null pointer");
@@ -237,6 +239,7 @@ int do_cpqr(spidgpu_handle h, Workspace& ws, const double* Y, int64_t rows, int6
 int do_gather(spidgpu_handle h, const double* A, int64_t m, int64_t n, int64_t lda, int64_t strideA,
               int64_t batch, const int64_t* indices, int64_t kcap, const int64_t* rank,
               double* skel, int64_t ldskel, int64_t strideS, cudaStream_t st) {
+    NvtxRange nvtx_range("spidgpu.gather");
     if (!A || !indices || !rank || !skel) return fail(h, SPID_INVALID_ARGUMENT, "null pointer");
     if (m < 1 || n < 1 || batch < 1 || kcap < 1) return fail(h, SPID_EMPTY_SELECTION, "empty gather");
     if (lda < m || ldskel < m) return fail(h, SPID_INVALID_ARGUMENT, "leading dimension too small");
@@ -252,6 +255,7 @@ int do_verify(spidgpu_handle h, Workspace& ws, const double* A, int64_t m, int64
               int64_t strideA, int64_t batch, const double* skel, int64_t ldskel, int64_t strideS,
               const double* C, int64_t kcap, int64_t strideC, const int64_t* rank, double* err2,
               double* ref2, cudaStream_t st) {
+    NvtxRange nvtx_range("spidgpu.verify");
     if (!A || !skel || !C || !rank || !err2 || !ref2)
         return fail(h, SPID_INVALID_ARGUMENT, "null pointer");
     if (kcap > 80) return fail(h, SPID_SHAPE_UNSUPPORTED, "verify supports rank <= 80");
@@ -517,6 +521,7 @@ const char* spidgpu_status_name(int status) {
         case SPID_UNSTRUCTURED_NO_INTERP: return "UnstructuredNoInterp";
         case SPID_BAD_STREAM_CONFIG: return "BadStreamConfig";
         case SPID_SHORT_STREAM: return "ShortStream";
+        case SPID_EMPTY_LOG: return "EmptyLog";
         case SPID_CUDA_ERROR: return "CudaError";
         case SPID_INVALID_ARGUMENT: return "InvalidArgument";
         case SPID_SHAPE_UNSUPPORTED: return "ShapeUnsupported";
@@ -731,6 +736,7 @@ int spidgpu_compress_batched(spidgpu_handle h, const double* A, int64_t m, int64
                              int64_t kcap, int64_t* indices, double* C, int64_t* rank,
                              double* residual_fro, int32_t* status, double* skel, double* Y,
                              void* stream) {
+    NvtxRange nvtx_range("spidgpu.compress_batched");
     if (!h) return SPID_INVALID_ARGUMENT;
     return do_compress(h, h->ws[0], A, m, n, lda, strideA, batch, ell, omega, rule, kcap, indices,
                        C, rank, residual_fro, status, skel, Y, static_cast<cudaStream_t>(stream));
@@ -941,6 +947,7 @@ int spidgpu_compress_host(spidgpu_handle h, const double* a, int64_t m, int64_t 
                           int64_t kcap, int64_t group, int64_t* indices, double* coeffs,
                           double* skel, int64_t* rank, double* residual_fro, int32_t* status,
                           double* err2, double* ref2) {
+    NvtxRange nvtx_range("spidgpu.compress_host");
     if (!h) return SPID_INVALID_ARGUMENT;
     if (m < 1 || n < 1 || batch < 1 || ell < 1) return fail(h, SPID_EMPTY_MATRIX, "empty batch");
     if (!a || !indices || !coeffs || !rank || !residual_fro || !status || !omega_ok(omega))

@@ -504,6 +504,7 @@ int spidgpu_crc32(spidgpu_handle h, const void* data, int64_t nbytes, int32_t on
 int spidgpu_archive_compress(spidgpu_handle h, const double* a, int64_t m, int64_t n, int64_t lda,
                              int32_t a_on_device, const spidgpu_archive_spec* spec,
                              const spidgpu_rank_rule* rule, int64_t* nbytes) {
+    NvtxRange nvtx_range("spidgpu.archive_compress");
     if (!h) return SPID_INVALID_ARGUMENT;
     if (!a || !spec || !rule || !nbytes) return fail(h, SPID_INVALID_ARGUMENT, "null argument");
     if (spec->mode != SPIDGPU_ARCHIVE_EXACT && spec->mode != SPIDGPU_ARCHIVE_SKETCH)
@@ -796,6 +797,7 @@ int spidgpu_archive_info(spidgpu_handle h, const uint8_t* bytes, int64_t nbytes,
 
 int spidgpu_archive_decompress(spidgpu_handle h, const uint8_t* bytes, int64_t nbytes, double* out,
                                int64_t ldo, int32_t out_on_device) {
+    NvtxRange nvtx_range("spidgpu.archive_decompress");
     if (!h) return SPID_INVALID_ARGUMENT;
     if (!bytes || !out || nbytes < 0) return fail(h, SPID_INVALID_ARGUMENT, "null argument");
     cudaSetDevice(h->device);

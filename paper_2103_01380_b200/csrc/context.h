@@ -3,6 +3,8 @@
 // the public interface (include/spidgpu.h).
 #pragma once
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -97,6 +99,16 @@ struct spidgpu_context {
 };
 
 namespace spidgpu {
+
+// NVTX phase ranges (header-only NVTX3: free unless a tool -- nsys, ncu
+// --nvtx -- injects a handler): every C-ABI phase of the compress path shows
+// up by name on a timeline, e.g. "spidgpu.sketch", "spidgpu.cpqr".
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 int fail(spidgpu_handle h, int code, const std::string& msg);
 int cuda_fail(spidgpu_handle h, cudaError_t e, const char* where);

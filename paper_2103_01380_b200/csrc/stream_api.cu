@@ -8,6 +8,7 @@
 // of chunk c and waits only when two chunks are in flight -- the reference's
 // backpressure bound (pipeline.cpp:184-189). Stage 2 and the archive run at
 // finish. The host never touches snapshot data.
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -54,6 +55,14 @@ struct spidgpu_stream {
     cudaStream_t s_in = nullptr, s_cmp = nullptr;
     cudaEvent_t ready = nullptr, free_ev[2] = {nullptr, nullptr};
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> s1_events;
+    // event log (spid::TaskEvent): device-timeline events
+    cudaEvent_t t0 = nullptr, f0 = nullptr, f1 = nullptr;  // open; stage 2 start / end
+    struct Push {
+        cudaEvent_t b, e;  // ingestion of frames [first, first + count) on s_in
+        int64_t first, count;
+    };
+    std::vector<Push> pushes;
+    std::vector<cudaEvent_t> closes;  // chunk c ingested (recorded before its stage 1)
     Workspace ws_cmp, ws_fin;
     // host frames land in alternating staging buffers: the gather of one push
     // (same stream, so ordered before the buffer's next copy) overlaps the
@@ -97,12 +106,17 @@ int sfail(spidgpu_stream* s, int code, const std::string& msg) {
 // Stage 1 of every block's closed chunk (pipeline.cpp:192-215 ->
 // stage1_compress_coarse, blocking.cpp:112-115).
 int close_chunk(spidgpu_stream* s) {
+    NvtxRange nvtx_range("spidgpu.stream.stage1");
     const int64_t cols = s->filled;
     if (cols == 0) return SPID_OK;
     const int64_t T = s->cfg.time_chunk;
     const int64_t kcap = std::min<int64_t>(s->cfg.stage1_rank, cols);
     SCK(s, cudaEventRecord(s->ready, s->s_in));
     SCK(s, cudaStreamWaitEvent(s->s_cmp, s->ready, 0));
+    cudaEvent_t ce;
+    SCK(s, cudaEventCreate(&ce));
+    SCK(s, cudaEventRecord(ce, s->s_in));
+    s->closes.push_back(ce);
     cudaEvent_t e0, e1;
     SCK(s, cudaEventCreate(&e0));
     SCK(s, cudaEventCreate(&e1));
@@ -147,6 +161,24 @@ int close_chunk(spidgpu_stream* s) {
     return SPID_OK;
 }
 
+// the begin / end events of one push on the ingestion stream (event log)
+struct Stream_push_log {
+    spidgpu_stream* s;
+    spidgpu_stream::Push p{};
+    Stream_push_log(spidgpu_stream* st, int64_t count) : s(st) {
+        p.first = s->snapshots;
+        p.count = count;
+        if (count > 0 && cudaEventCreate(&p.b) == cudaSuccess) cudaEventRecord(p.b, s->s_in);
+    }
+    ~Stream_push_log() {
+        if (!p.b) return;
+        if (cudaEventCreate(&p.e) == cudaSuccess && cudaEventRecord(p.e, s->s_in) == cudaSuccess)
+            s->pushes.push_back(p);
+        else
+            cudaEventDestroy(p.b);
+    }
+};
+
 void destroy(spidgpu_stream* s) {
     if (s->s_cmp) cudaStreamSynchronize(s->s_cmp);
     if (s->s_in) cudaStreamSynchronize(s->s_in);
@@ -168,6 +200,13 @@ void destroy(spidgpu_stream* s) {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
     }
+    for (auto& p : s->pushes) {
+        cudaEventDestroy(p.b);
+        cudaEventDestroy(p.e);
+    }
+    for (cudaEvent_t e : s->closes) cudaEventDestroy(e);
+    for (cudaEvent_t e : {s->t0, s->f0, s->f1})
+        if (e) cudaEventDestroy(e);
     if (s->ready) cudaEventDestroy(s->ready);
     for (cudaEvent_t e : s->free_ev)
         if (e) cudaEventDestroy(e);
@@ -219,7 +258,8 @@ int spidgpu_stream_open(spidgpu_handle h, const spidgpu_stream_config* cfg, spid
         cudaEventCreateWithFlags(&s->ready, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&s->free_ev[0], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&s->free_ev[1], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&s->copied, cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&s->copied, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreate(&s->t0) != cudaSuccess || cudaEventRecord(s->t0, s->s_in) != cudaSuccess)
         return bail(fail(h, SPID_CUDA_ERROR, "stream/event creation failed"));
     for (const Group& G : group_blocks(s->L, nullptr)) {
         SGroup g;
@@ -258,6 +298,7 @@ int spidgpu_stream_push(spidgpu_stream_handle s, const double* frames, int64_t m
     if (count > 0 && ld < m) return sfail(s, SPID_INVALID_ARGUMENT, "ld < m");
     cudaSetDevice(s->h->device);
     const int64_t T = s->cfg.time_chunk;
+    Stream_push_log log(s, count);
     for (int64_t j = 0; j < count;) {
         const int64_t c = std::min(count - j, T - s->filled);
         const double* src = frames + j * ld;
@@ -295,6 +336,7 @@ int spidgpu_stream_push(spidgpu_stream_handle s, const double* frames, int64_t m
 }
 
 int spidgpu_stream_finish(spidgpu_stream_handle s, int64_t* nbytes) {
+    NvtxRange nvtx_range("spidgpu.stream.finish");
     if (!s) return SPID_INVALID_ARGUMENT;
     if (!nbytes) return sfail(s, SPID_INVALID_ARGUMENT, "null nbytes");
     if (s->finished) return sfail(s, SPID_INVALID_ARGUMENT, "stream already finished");
@@ -332,9 +374,9 @@ int spidgpu_stream_finish(spidgpu_stream_handle s, int64_t* nbytes) {
     }
 
     // ---- stage 2 per geometry group (blocking.cpp:128-204) ---------------------------------
-    cudaEvent_t f0, f1;
-    SCK(s, cudaEventCreate(&f0));
-    SCK(s, cudaEventCreate(&f1));
+    SCK(s, cudaEventCreate(&s->f0));
+    SCK(s, cudaEventCreate(&s->f1));
+    cudaEvent_t f0 = s->f0, f1 = s->f1;
     SCK(s, cudaEventRecord(f0, s->s_cmp));
     spidgpu_rank_rule rule2{SPIDGPU_RULE_TOL, 0, 0, 0, s->cfg.stage2_tol};
     struct Fin {
@@ -486,8 +528,75 @@ int spidgpu_stream_finish(spidgpu_stream_handle s, int64_t* nbytes) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, f0, f1);
     s->stage2_ms = ms;
-    cudaEventDestroy(f0);
-    cudaEventDestroy(f1);
+    return SPID_OK;
+}
+
+int spidgpu_stream_events(spidgpu_stream_handle s, spidgpu_task_event* out, int64_t cap, int64_t* count) {
+    if (!s || !count || (cap > 0 && !out)) return SPID_INVALID_ARGUMENT;
+    if (!s->finished || !s->f1) return sfail(s, SPID_INVALID_ARGUMENT, "the event log is complete after finish");
+    cudaSetDevice(s->h->device);
+    SCK(s, cudaEventSynchronize(s->f1));
+    auto at = [&](cudaEvent_t e) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, s->t0, e);
+        return 1e-3 * ms;
+    };
+    auto span = [&](cudaEvent_t a, cudaEvent_t b) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        return 1e-3 * ms;
+    };
+    const int64_t nblocks = static_cast<int64_t>(s->L.doms.size());
+    std::vector<spidgpu_task_event> ev;
+    for (const auto& p : s->pushes)
+        for (int64_t j = 0; j < p.count; ++j)
+            ev.push_back({SPIDGPU_EVENT_SNAPSHOT_INGESTED, -1, p.first + j, at(p.e), span(p.b, p.e)});
+    for (size_t c = 0; c < s->closes.size(); ++c)
+        for (int64_t b = 0; b < nblocks; ++b)
+            ev.push_back({SPIDGPU_EVENT_CHUNK_CLOSED, b, static_cast<int64_t>(c), at(s->closes[c]), 0.0});
+    for (size_t c = 0; c < s->s1_events.size(); ++c)
+        for (int64_t b = 0; b < nblocks; ++b)
+            ev.push_back({SPIDGPU_EVENT_STAGE1_DONE, b, static_cast<int64_t>(c), at(s->s1_events[c].second),
+                          span(s->s1_events[c].first, s->s1_events[c].second)});
+    for (int64_t b = 0; b < nblocks; ++b)
+        ev.push_back({SPIDGPU_EVENT_STAGE2_DONE, b, -1, at(s->f1), span(s->f0, s->f1)});
+    *count = static_cast<int64_t>(ev.size());
+    for (int64_t i = 0; i < cap && i < *count; ++i) out[i] = ev[static_cast<size_t>(i)];
+    return SPID_OK;
+}
+
+// Merged producer (ingestion) intervals, then the stage-1 time inside them,
+// in the reference's order of operations (pipeline.cpp:296-332).
+int spidgpu_overlap_report(const spidgpu_task_event* events, int64_t count, spidgpu_overlap* out) {
+    if (!out || (count > 0 && !events)) return SPID_INVALID_ARGUMENT;
+    if (count <= 0) return SPID_EMPTY_LOG;
+    std::vector<std::pair<double, double>> producer, stage1, merged;
+    for (int64_t i = 0; i < count; ++i) {
+        const spidgpu_task_event& e = events[i];
+        if (e.kind == SPIDGPU_EVENT_SNAPSHOT_INGESTED)
+            producer.emplace_back(e.wall_time - e.duration, e.wall_time);
+        else if (e.kind == SPIDGPU_EVENT_STAGE1_DONE)
+            stage1.emplace_back(e.wall_time - e.duration, e.wall_time);
+    }
+    std::sort(producer.begin(), producer.end());
+    for (const auto& iv : producer) {
+        if (!merged.empty() && iv.first <= merged.back().second)
+            merged.back().second = std::max(merged.back().second, iv.second);
+        else
+            merged.push_back(iv);
+    }
+    spidgpu_overlap r{0.0, 0.0, 0.0};
+    for (const auto& iv : merged) r.producer_busy_seconds += iv.second - iv.first;
+    double overlap = 0.0;
+    for (const auto& iv : stage1) {
+        r.stage1_busy_seconds += iv.second - iv.first;
+        for (const auto& pv : merged) {
+            const double lo = std::max(iv.first, pv.first), hi = std::min(iv.second, pv.second);
+            if (hi > lo) overlap += hi - lo;
+        }
+    }
+    r.overlap_fraction = r.stage1_busy_seconds > 0.0 ? overlap / r.stage1_busy_seconds : 0.0;
+    *out = r;
     return SPID_OK;
 }
 

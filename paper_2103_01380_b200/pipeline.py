@@ -23,7 +23,31 @@ import numpy as np
 from . import _native as N
 from ._native import SpidError
 
-__all__ = ["StreamConfig", "Pipeline", "run_pipeline"]
+__all__ = ["StreamConfig", "Pipeline", "run_pipeline", "TaskEvent", "overlap_report"]
+
+
+@dataclass
+class TaskEvent:
+    """spid::TaskEvent (proj/include/spid/pipeline.hpp:24-32); times in
+    seconds on the device timeline from the stream's open."""
+    kind: str       # SnapshotIngested | ChunkClosed | Stage1Done | Stage2Done
+    block: int
+    chunk: int
+    wall_time: float
+    duration: float
+
+
+def overlap_report(events) -> dict:
+    """spid::overlap_report (proj/src/pipeline.cpp:296-332): the fraction of
+    stage-1 time that ran while ingestion was busy."""
+    arr = (N.TaskEvent * max(1, len(events)))()
+    for i, e in enumerate(events):
+        arr[i] = N.TaskEvent(N.EVENT_KINDS.index(e.kind), e.block, e.chunk, e.wall_time, e.duration)
+    out = N.Overlap()
+    rc = N.lib.spidgpu_overlap_report(arr, len(events), C.byref(out))
+    if rc:
+        raise SpidError(N.status_name(rc), "overlap_report")
+    return {k: getattr(out, k) for k, _ in N.Overlap._fields_}
 
 
 @dataclass
@@ -95,6 +119,15 @@ class Pipeline:
         st = N.StreamStats()
         self._check(N.lib.spidgpu_stream_get_stats(self.s, C.byref(st)))
         return {k: getattr(st, k) for k, _ in N.StreamStats._fields_}
+
+    def events(self) -> list:
+        """The event log (PipelineResult.events) -- after finish()."""
+        n = C.c_int64()
+        self._check(N.lib.spidgpu_stream_events(self.s, None, 0, C.byref(n)))
+        arr = (N.TaskEvent * max(1, n.value))()
+        self._check(N.lib.spidgpu_stream_events(self.s, arr, n.value, C.byref(n)))
+        return [TaskEvent(N.EVENT_KINDS[e.kind], e.block, e.chunk, e.wall_time, e.duration)
+                for e in arr[:n.value]]
 
     def close(self):
         if getattr(self, "s", None):

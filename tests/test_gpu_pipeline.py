@@ -144,3 +144,45 @@ def test_large_stream_vs_reference(PL, ref):
     theirs, _ = ref.run_pipeline(a, (g,) * 3, (4, 4, 4), (2, 2, 2), 16, 6, 1e-5, periodic=(1, 1, 1), qoi="u",
                                  provenance="large")
     assert ours == theirs
+
+
+def test_event_log_causality_and_counts(PL):
+    """PipelineResult.events (proj/include/spid/pipeline.hpp:24-60): one
+    SnapshotIngested per frame, ChunkClosed / Stage1Done per (block, chunk),
+    Stage2Done per block; every chunk closes before its stage 1 completes and
+    every stage 1 completes before stage 2 (proj/tests/test_pipeline.cpp:127)."""
+    rng = np.random.default_rng(33)
+    dims, blocks, T, n = (16, 12), (2, 2), 4, 14
+    a = np.asfortranarray(rng.standard_normal((16 * 12, 2)) @ rng.standard_normal((2, n)))
+    cfg = PL.StreamConfig(dims=dims, blocks=blocks, strides=(2, 2), time_chunk=T, stage1_rank=2, stage2_tol=1e-6)
+    with PL.Pipeline(cfg) as p:
+        for j in range(0, n, 3):
+            p.push(a[:, j:j + 3])
+        p.finish()
+        ev = p.events()
+    nb, nch = 4, -(-n // T)
+    kinds = [e.kind for e in ev]
+    assert kinds.count("SnapshotIngested") == n
+    assert sorted(e.chunk for e in ev if e.kind == "SnapshotIngested") == list(range(n))
+    assert kinds.count("ChunkClosed") == nb * nch and kinds.count("Stage1Done") == nb * nch
+    assert kinds.count("Stage2Done") == nb
+    closed = {(e.block, e.chunk): e.wall_time for e in ev if e.kind == "ChunkClosed"}
+    done = {(e.block, e.chunk): e.wall_time for e in ev if e.kind == "Stage1Done"}
+    stage2 = min(e.wall_time for e in ev if e.kind == "Stage2Done")
+    assert set(closed) == set(done)
+    for key, t in done.items():
+        assert closed[key] <= t <= stage2
+    for e in ev:
+        assert e.duration >= 0.0 and e.wall_time >= e.duration
+    rep = PL.overlap_report(ev)
+    assert 0.0 <= rep["overlap_fraction"] <= 1.0 and rep["stage1_busy_seconds"] > 0.0
+    # the reference's arithmetic on a hand-made log (pipeline.cpp:296-332)
+    mk = lambda k, t, d: PL.TaskEvent(k, -1, 0, t, d)  # noqa: E731
+    r = PL.overlap_report([mk("SnapshotIngested", 2.0, 1.0), mk("SnapshotIngested", 2.5, 1.0),
+                           mk("SnapshotIngested", 5.0, 0.5), mk("Stage1Done", 3.0, 2.0)])
+    assert r["producer_busy_seconds"] == pytest.approx(1.5 + 0.5)
+    assert r["stage1_busy_seconds"] == pytest.approx(2.0)
+    assert r["overlap_fraction"] == pytest.approx(1.5 / 2.0)
+    with pytest.raises(PL.SpidError) as e:
+        PL.overlap_report([])
+    assert e.value.name == "EmptyLog"
