@@ -351,6 +351,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kAStages = Cfg::kASt;
     constexpr int kAStageBytes = Cfg::kAStB;
     constexpr int kStageRows = Cfg::kStageRows, kKB = Cfg::kKB, kTileBytes = Cfg::kTileBytes;
+    // Omega tile tasks (one Philox call = one octet, or two for a 16-byte K
+    // half when the tile has more octets than generator lanes), split over
+    // the cluster's CTAs, at most one per lane, on as few warps as that takes
+    // (a warp's instructions per stage do not shrink with idle lanes: -3%
+    // cycles at ell 64 and 80)
+    constexpr int kOctets = kStageRows / 8;  // per Omega row and stage
+    constexpr bool kFine = kOctets * NPAD <= 32 * kGenWarps * P;
+    constexpr int kTasks = kFine ? kOctets * NPAD : kOctets / 2 * NPAD;
+    constexpr int kTasksCta = kTasks / P;
+    constexpr int kGenNeed = (kTasksCta + 31) / 32 < 1 ? 1 : (kTasksCta + 31) / 32;
+    constexpr int kGenActive = kGenNeed < kGenWarps ? kGenNeed : kGenWarps;
     extern __shared__ unsigned char smem_raw[];
     const uint32_t raw_s = smem_u32(smem_raw);
     const uint32_t base_s = (raw_s + 1023u) & ~1023u;
@@ -391,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (kSplit)  // the mailboxes' first phases: the peer's 128 column maxima of stages 0..
             for (int i = 0; i < kAStages; ++i) mbar_arrive_expect_tx(&m_full[i], kM * 4);
         for (int i = 0; i < kBStages; ++i) {
-            mbar_init(&b_full[i], kConvWarps + kGenWarps);
+            mbar_init(&b_full[i], kConvWarps + kGenActive);
             mbar_init(&b_empty[i], P);  // MMA commits of this CTA (and of its peer)
         }
         fence_barrier_init();
@@ -420,11 +431,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // most one task per stage, so the tile's latency is one task's.
         // A pair splits the tile's tasks: this CTA runs [rank, rank + 1) x
         // kTasksCta of them and also writes them into the peer's tile.
-        constexpr int kOctets = kStageRows / 8;  // per Omega row and stage
-        constexpr bool kFine = kOctets * NPAD <= 32 * kGenWarps * P;
-        constexpr int kTasks = kFine ? kOctets * NPAD : kOctets / 2 * NPAD;
-        constexpr int kTasksCta = kTasks / P;
-        constexpr int kTasksPerWarp = (kTasksCta + kGenWarps - 1) / kGenWarps;
+        // (task decomposition at the top of the kernel: kFine, kTasksCta, kGenActive)
+        constexpr int kTasksPerWarp = (kTasksCta + kGenActive - 1) / kGenActive;
         constexpr uint32_t kPeerBytes = kTasksCta * (kFine ? 8 : 16);  // Omega bytes the peer sends per stage
         static_assert(kTasksPerWarp <= 32, "one Omega task per lane");
         const int gw = warp == 0 ? 0 : warp - 1;
@@ -494,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     else if (++sp == sl) sp = 0;
                 }
             }
-        } else
+        } else if (gw < kGenActive)  // warp 0 (gw 0, the TMA producer) always runs the loop
         for (int it = 0; it < niter; ++it) {
             const int sl = it % kBStages;
             const uint32_t ot = b_s + sl * Cfg::kBStageBytes + kSl * kTileBytes;
