@@ -264,8 +264,18 @@ __global__ void __launch_bounds__(256) sketch_reduce_kernel(SketchParams p, int 
     for (int e = threadIdx.x; e < nrows * ncols; e += blockDim.x) {
         const int rl = e / ncols, col = e % ncols;  // column fastest: coalesced partial reads
         const double* src = tpart + (r0 + rl) * nt + col;
+        // segment order (the fixed association); loads batched 8 ahead of the adds
+        const int64_t ng = nseg * halves;
         double sum = 0.0;
-        for (int64_t g = 0; g < nseg * halves; ++g) sum += src[g * slot_elems];
+        int64_t g = 0;
+        for (; g + 8 <= ng; g += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldcs(src + (g + u) * slot_elems);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) sum += v[u];
+        }
+        for (; g < ng; ++g) sum += __ldcs(src + g * slot_elems);
         slab[rl][col] = sum;
     }
     __syncthreads();

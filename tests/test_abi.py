@@ -113,3 +113,18 @@ def test_cpp_shim_compiles():
     assert r.returncode == 0, r.stderr
     r = subprocess.run([out, "--no-device-ok"], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_cpp_shim_runs_on_device():
+    """The same shim program with a device: the reference's TGV rank-1 known
+    answer (proj/tests/acceptance.cpp:77-114) through spidgpu::column_id,
+    reconstruct and rel_frob_error on the B200."""
+    src = os.path.join(ROOT, "tools", "shim_check.cpp")
+    out = "/tmp/spidgpu_shim_check_dev"
+    lib = os.path.join(ROOT, "paper_2103_01380_b200", "lib")
+    r = subprocess.run(["g++", "-std=c++17", "-O1", f"-I{ROOT}/include", src, "-o", out,
+                        f"-L{lib}", "-lspidgpu", f"-Wl,-rpath,{lib}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([out], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
