@@ -192,6 +192,13 @@ __device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t adesc, uint64_
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// one lane of a converged warp
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                      smem_u32(bar))
@@ -450,7 +457,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t acc = seg_pos != 0 ? 1u : 0u;
             const uint32_t st = b_s + sl * Cfg::kBStageBytes;
             const uint32_t ot = st + kSl * kTileBytes;  // Omega tile: K blocks of NPAD x 32 bytes
-            if constexpr (!kSplit) {
+            if (!elect_one()) {
+            } else if constexpr (!kSplit) {
                 const uint64_t bdesc = smem_desc(ot, NPAD * 16, 128);
 #pragma unroll
                 for (int t = 0; t < kSlices; ++t)
@@ -470,10 +478,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 bdesc, kIdU, kb > 0 ? 1u : acc);
                 }
             }
-            if constexpr (kPair)
-                umma_commit_pair(&b_empty[sl]);
-            else
-                umma_commit(&b_empty[sl]);
+            __syncwarp();
+            if (elect_one()) {
+                if constexpr (kPair)
+                    umma_commit_pair(&b_empty[sl]);
+                else
+                    umma_commit(&b_empty[sl]);
+            }
+            __syncwarp();
         };
         ChunkPos cp = chunk_pos(lo, nchunk, ntiles_col);
         ChunkPos tp = cp;  // TMA position (warp 0)
@@ -492,15 +504,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (warp == 0 && lane == 0)
             for (int it = 0; it < kAStages && it < niter; ++it) issue_tma(it);
         if (warp == 1) {  // dedicated MMA issuer: no Omega work, so MMAs go out as soon as a stage is full
-            if (lane == 0) {
-                // position inside the current segment (ranges start on segment starts)
-                int sp = 0, kc = cp.kc;
-                const int nch = static_cast<int>(nchunk), sl = static_cast<int>(seg_len);
-                for (int it = 0; it < niter; ++it) {
-                    issue_mma(it, sp);
-                    if (++kc == nch) kc = sp = 0;
-                    else if (++sp == sl) sp = 0;
-                }
+            // the whole warp runs the loop (warp-uniform values stay in
+            // uniform registers); one elected lane issues the MMAs
+            // position inside the current segment (ranges start on segment starts)
+            int sp = 0, kc = cp.kc;
+            const int nch = static_cast<int>(nchunk), sl = static_cast<int>(seg_len);
+            for (int it = 0; it < niter; ++it) {
+                issue_mma(it, sp);
+                if (++kc == nch) kc = sp = 0;
+                else if (++sp == sl) sp = 0;
             }
         } else if (gw < kGenActive)  // warp 0 (gw 0, the TMA producer) always runs the loop
         for (int it = 0; it < niter; ++it) {
