@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kMode == 2 ? kCpqrThreads + kWarp : kCpqrThrea
         cur += sizeof(int) * n;
         posof = reinterpret_cast<int*>(cur);
         cur += sizeof(int) * n;
-        cur = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(cur) + 15) & ~uintptr_t(15));
+        cur = smem_raw + ((cur - smem_raw + 15) & ~ptrdiff_t(15));  // stays a shared-window pointer
         diag = reinterpret_cast<double*>(cur);
         cur += sizeof(double) * p.step_cap;
         if (kWInShared) {

@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
     __shared__ double red_v[kT / kWarp];
     __shared__ int red_i[kT / kWarp];
     __shared__ __align__(16) double qbuf[ROWS + 2];
-    const uint32_t qs = smem_u32(qbuf);
+    const double2* q2 = reinterpret_cast<const double2*>(qbuf);
 
     const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < ROWS + 2; i += kT) qbuf[i] = 0.0;  // rows..ROWS stay zero
@@ -47,8 +47,10 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
     double* diag = colsq + n;
     int* perm = reinterpret_cast<int*>(diag + cap);
     int* posof = perm + n;
-    double* X = reinterpret_cast<double*>(
-        (reinterpret_cast<uintptr_t>(posof + n) + 15) & ~uintptr_t(15));
+    // offsets from smem_raw (not integer-cast pointers) keep the shared
+    // window visible to the compiler: LDS/STS instead of generic accesses
+    const size_t x_off = (reinterpret_cast<unsigned char*>(posof + n) - smem_raw + 15) & ~size_t(15);
+    double* X = reinterpret_cast<double*>(smem_raw + x_off);
     double* r11 = X + static_cast<size_t>(cap) * n;
     double* R = p.r_ws + static_cast<size_t>(b) * cap * n;  // R[s][col], global
     const double* Y = p.Y + static_cast<size_t>(b) * p.strideY;
@@ -226,25 +228,29 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
         for (int c = 0; c < CPT; ++c) {
             const int j = tid + c * kT;
             if (alive[c]) {
-                // q is re-read (16-byte broadcast LDS, opaque to the compiler)
-                // in every pass instead of being cached: keeps the register
-                // budget to the column itself. Rows past `rows` are +0.0 in
-                // both q and w and stay +0.0 (0 - r*0 = +0), so the padded
-                // terms add +0.0 to sums that cannot be -0.0: bit-neutral,
-                // and the loops carry no per-element branches.
+                // q is re-read (16-byte broadcast loads) in every pass
+                // instead of being cached across passes (the compiler fence
+                // between passes): keeps the register budget to the column
+                // itself, while inside a pass the loads are ordinary reads
+                // the compiler issues ahead of the dependent chain. Rows past
+                // `rows` are +0.0 in both q and w and stay +0.0 (0 - r*0 =
+                // +0), so the padded terms add +0.0 to sums that cannot be
+                // -0.0: bit-neutral, and the loops carry no per-element
+                // branches.
                 double r1 = 0.0;
 #pragma unroll
                 for (int i = 0; i < ROWS; i += 2) {
                     if (!kFree && i >= rows) break;
-                    const double2 q = lds128(qs + 16 * (i / 2));
+                    const double2 q = q2[i / 2];
                     r1 = add_rn(r1, mul_rn(q.x, w[c][i]));
                     r1 = add_rn(r1, mul_rn(q.y, w[c][i + 1]));
                 }
+                asm volatile("" ::: "memory");
                 double r2 = 0.0;
 #pragma unroll
                 for (int i = 0; i < ROWS; i += 2) {
                     if (!kFree && i >= rows) break;
-                    const double2 q = lds128(qs + 16 * (i / 2));
+                    const double2 q = q2[i / 2];
                     const double v0 = sub_rn(w[c][i], mul_rn(r1, q.x));
                     w[c][i] = v0;
                     r2 = add_rn(r2, mul_rn(q.x, v0));
@@ -252,11 +258,12 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
                     w[c][i + 1] = v1;
                     r2 = add_rn(r2, mul_rn(q.y, v1));
                 }
+                asm volatile("" ::: "memory");
                 double nn = 0.0;
 #pragma unroll
                 for (int i = 0; i < ROWS; i += 2) {
                     if (!kFree && i >= rows) break;
-                    const double2 q = lds128(qs + 16 * (i / 2));
+                    const double2 q = q2[i / 2];
                     const double v0 = sub_rn(w[c][i], mul_rn(r2, q.x));
                     w[c][i] = v0;
                     nn = add_rn(nn, mul_rn(v0, v0));
