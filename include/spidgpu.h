@@ -91,10 +91,11 @@ int64_t spidgpu_launch_count(spidgpu_handle h);
  * SPIDGPU_OPT_SKETCH_SMS = 4 caps the SMs the persistent sketch kernels
  * occupy (0 = all), leaving the rest to kernels on other streams (the
  * overlapped compress pipeline).
- * SPIDGPU_OPT_SKETCH_PAIRS = 5 runs the tcgen05 sketch as clusters of two
- * CTAs that share each stage's Omega tile: 0 never, 1 (default) where it
- * measured faster (64-row passes), 2 whenever the column tiles pair up
- * (bitwise the same Y; tests and A/B).
+ * SPIDGPU_OPT_SKETCH_PAIRS = 5 runs the tcgen05 sketch of up to 64 rows as
+ * clusters of two CTAs that share each stage's Omega tile: 0 and 1 (default)
+ * never (one CTA per tile measured as fast or faster at every width), 2
+ * whenever the column tiles pair up (bitwise the same Y; tests and A/B).
+ * Sketches of 65-80 rows always run as slice-split CTA pairs.
  * Every sketch is bitwise independent of the batch it runs in, the SM cap,
  * the pair mode and the GPU count: work is split at fixed 4096-row segment
  * boundaries and segment partials are summed in a fixed order.

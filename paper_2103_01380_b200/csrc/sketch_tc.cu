@@ -917,17 +917,19 @@ bool sketch_tc_make_plan(int64_t m, int64_t n, int64_t batch, int64_t ell, int n
     // the sketch into passes of <= 64 rows instead.
     // Otherwise CTA pairs (mode 1) when the column tiles pair up and the
     // device keeps at least as many pairs resident as half the SM budget
-    // (clusters of two span a TPC). pair_mode 1 (default) pairs only ell_pad
-    // 64, where halving the Omega work outweighs the pair's lock-step (base
-    // clock, config 3: -3% at 64, +4.5% at 48, +8% at 16); 2 pairs whenever
-    // possible (tests, A/B).
+    // (clusters of two span a TPC), only with pair_mode 2 (tests, A/B): since
+    // the MMA warp issues through elect.sync, one CTA per tile is as fast or
+    // faster at every width (config-3 batch, same-process A/B: ell 64 4.36 vs
+    // 4.47 ms, 48 3.69 vs 3.87, 32 3.65 vs 3.87 -- the pair's lock-step costs
+    // more than halving the Omega work saves). pair_mode 0 and 1 (default)
+    // never pair.
     int pairs = 0;
     if (plan->ell_pad == 80) {
         pairs = num_sms >= 2 ? max_pairs_for(80, 2) : 0;
         if (pairs == 0) return false;
         plan->pair = 2;
     } else {
-        const bool want = pair_mode == 2 || (pair_mode == 1 && plan->ell_pad == 64);
+        const bool want = pair_mode == 2;
         pairs = want && num_sms >= 2 && plan->ntiles_col % 2 == 0 ? max_pairs_for(plan->ell_pad, 1) : 0;
         plan->pair = pairs > 0 && 2 * pairs >= num_sms - 1 ? 1 : 0;
     }

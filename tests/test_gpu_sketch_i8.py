@@ -59,8 +59,8 @@ def _pairs(engine, mode):
 
 @pytest.fixture(params=["tc", "tc_pairs"], autouse=True)
 def kernel(request, engine):
-    """tcgen05 sketch with CTA pairs only for 64-row passes (the default), or
-    with CTA pairs wherever the column tiles pair up."""
+    """tcgen05 sketch with one CTA per column tile for up to 64 rows (the
+    default), or with CTA pairs wherever the column tiles pair up."""
     _pairs(engine, 2 if request.param == "tc_pairs" else 1)
     yield request.param
     _pairs(engine, 1)
