@@ -69,6 +69,11 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
     // larger tiles exit at `rows` (a uniform branch) to keep registers down.
     // Both are bit-identical: padded rows only ever contribute +0.0.
     constexpr bool kFree = ROWS * CPT <= 48;
+    // MGS passes of larger tiles stop at the first whole group of kGrp rows
+    // past `rows` (the padded rows in between are +0.0: bit-neutral), so the
+    // compiler schedules each group's independent products ahead of its
+    // dependent adds instead of branching per element
+    constexpr int kGrp = 16;
     int bad = 0;
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
@@ -240,7 +245,7 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
                 double r1 = 0.0;
 #pragma unroll
                 for (int i = 0; i < ROWS; i += 2) {
-                    if (!kFree && i >= rows) break;
+                    if (!kFree && i % kGrp == 0 && i >= rows) break;
                     const double2 q = q2[i / 2];
                     r1 = add_rn(r1, mul_rn(q.x, w[c][i]));
                     r1 = add_rn(r1, mul_rn(q.y, w[c][i + 1]));
@@ -249,7 +254,7 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
                 double r2 = 0.0;
 #pragma unroll
                 for (int i = 0; i < ROWS; i += 2) {
-                    if (!kFree && i >= rows) break;
+                    if (!kFree && i % kGrp == 0 && i >= rows) break;
                     const double2 q = q2[i / 2];
                     const double v0 = sub_rn(w[c][i], mul_rn(r1, q.x));
                     w[c][i] = v0;
@@ -262,7 +267,7 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
                 double nn = 0.0;
 #pragma unroll
                 for (int i = 0; i < ROWS; i += 2) {
-                    if (!kFree && i >= rows) break;
+                    if (!kFree && i % kGrp == 0 && i >= rows) break;
                     const double2 q = q2[i / 2];
                     const double v0 = sub_rn(w[c][i], mul_rn(r2, q.x));
                     w[c][i] = v0;
