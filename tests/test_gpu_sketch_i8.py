@@ -294,6 +294,24 @@ def test_large_subdomain_cfg3_shape(engine, spid):
     _check(engine, spid, A, cfg.ell, seed=cfg.seed, base=5, exact=False)
 
 
+def test_large_subdomain_cfg4_shape(engine, spid):
+    """One config-4 heavy subdomain (163840 x 256, +256 high-wavenumber
+    modes), ell = 80 in one pass (slice-split CTA pairs, 20 segments of 8192
+    rows, two partials each), against the oracle's fp64 matmul within the
+    contract + gamma_m; and bitwise the same Y when sketched inside a batch
+    of four."""
+    import numpy as np
+
+    from paper_2103_01380_b200.configs import CONFIGS
+
+    cfg = CONFIGS["cfg4"]
+    heavy = np.array([0, 1, 1, 0], dtype=np.uint8)
+    A = engine.generate(cfg, 0, 4, heavy=heavy)
+    Y1, _ = _check(engine, spid, A[1:2].contiguous(), cfg.ell, seed=cfg.seed, base=1, exact=False)
+    Y4 = engine.sketch(A, cfg.ell, seed=cfg.seed, subdomain_base=0)
+    assert torch.equal(Y4[1:2], Y1)
+
+
 def test_padded_leading_dimension_and_stride(engine, spid):
     """lda > m and strideA > lda*n (a padded, strided batch) through the C ABI:
     the TMA tensor map walks the strides, padding rows are never read."""
