@@ -10,7 +10,7 @@
 //
 // Layout of the work (mirrors sketch.cu):
 //  * persistent grid, one CTA per SM, contiguous ranges of whole
-//    (subdomain, column tile, 4096-row segment) units (as the sketch,
+//    (subdomain, column tile, 2048-row segment) units (as the sketch,
 //    kernels.h), so the sums do not depend on the batch or the grid;
 //  * 1 producer warp issues two TMA boxes per chunk -- A (16 rows x NT
 //    columns) and the skeleton rows (16 rows x 4*KS columns), both 128B
@@ -33,6 +33,11 @@ namespace spidgpu {
 namespace {
 
 constexpr int kRows = 16;          // rows per chunk (one 128 B swizzle row)
+// verify's fixed segments (batch independence, as the sketch's): 2048 rows --
+// twice the units of 4096 evens out the per-CTA unit counts (config 3: 34.6
+// instead of 17.3 units per CTA; 6.43 vs 6.55 ms), 1024 adds more segment
+// flushes than it saves (6.53 ms)
+constexpr int64_t kVerifySegRows = 2048;
 constexpr int kCons = 8;           // consumer warps (2 per SMSP: 170 registers each)
 constexpr int kThreadsV = (kCons + 1) * kWarp;
 constexpr int kBudget = 200 * 1024;
@@ -281,7 +286,7 @@ bool verify_make_plan(int64_t m, int64_t n, int64_t batch, int64_t kcap, int num
     plan->nt = kCons * 8 * nwv;
     plan->ntiles_col = (n + plan->nt - 1) / plan->nt;
     plan->nchunk = (m + kRows - 1) / kRows;
-    plan->seg_len = kSketchSegRows / kRows;
+    plan->seg_len = kVerifySegRows / kRows;
     plan->nseg = (plan->nchunk + plan->seg_len - 1) / plan->seg_len;
     plan->total_units = batch * plan->ntiles_col * plan->nseg;
     int64_t grid = num_sms;
