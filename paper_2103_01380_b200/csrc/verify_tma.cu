@@ -136,6 +136,10 @@ __global__ void __launch_bounds__(kThreadsV, 1)
     double err = 0.0, ref = 0.0;
     int slot = 0;
     uint32_t par = 0;
+    // segment bookkeeping by counters (no 64-bit division per chunk); ranges
+    // start on segment starts
+    int64_t sg = kc / seg_len;                       // segment of the current chunk
+    int64_t seg_left = seg_len;                      // chunks left in it
     for (int64_t it = 0; it < niter; ++it) {
         mbar_wait(&full[slot], par);
         const uint32_t at = a_s + slot * Cfg::kABytes;
@@ -188,7 +192,7 @@ __global__ void __launch_bounds__(kThreadsV, 1)
             slot = 0;
             par ^= 1u;
         }
-        if (kc + 1 == nchunk || (kc + 1) % seg_len == 0) {  // segment end: flush this warp's sums
+        if (kc + 1 == nchunk || --seg_left == 0) {  // segment end: flush this warp's sums
             double e2 = err, r2 = ref;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) {
@@ -196,14 +200,18 @@ __global__ void __launch_bounds__(kThreadsV, 1)
                 r2 += __shfl_xor_sync(0xffffffffu, r2, off);
             }
             if (lane == 0) {
-                double* dst = part + ((static_cast<size_t>(tile) * nseg + kc / seg_len) * kCons + warp) * 2;
+                double* dst = part + ((static_cast<size_t>(tile) * nseg + sg) * kCons + warp) * 2;
                 dst[0] = e2;
                 dst[1] = r2;
             }
             err = ref = 0.0;
+            ++sg;
+            seg_left = seg_len;
         }
         if (++kc == nchunk) {
             kc = 0;
+            sg = 0;
+            seg_left = seg_len;
             ++tile;
             if (it + 1 < niter) load_tile(tile);
         }
