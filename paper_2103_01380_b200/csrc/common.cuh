@@ -14,6 +14,18 @@ constexpr int kWarp = 32;
 // reference is built for x86-64 without -march, so every `s += x*y` there is
 // a rounded multiply followed by a rounded add (proj/src/dense_matrix.cpp:
 // 136-140); these wrappers reproduce that bit-for-bit.
+// Launch grid of the column gathers: x covers a column's rows (256-thread
+// blocks, at most 32 per column), y the columns, grid-striding so the whole
+// grid stays near 4096 blocks (148 SMs x ~28)
+inline dim3 col_grid(int64_t nrows, int64_t ncols) {
+    int64_t x = (nrows + 255) / 256;
+    if (x > 32) x = 32;
+    if (x < 1) x = 1;
+    const int64_t ycap = 4096 / x;
+    const int64_t y = ncols < 1 ? 1 : (ncols > ycap ? ycap : ncols);
+    return dim3(static_cast<unsigned>(x), static_cast<unsigned>(y));
+}
+
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }

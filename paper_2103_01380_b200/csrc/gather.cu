@@ -55,16 +55,18 @@ __global__ void gather_rows_kernel(const double* __restrict__ A, int64_t m, int6
                                    int64_t lda, int64_t strideA, int64_t batch,
                                    const int64_t* __restrict__ rows, int64_t nrows,
                                    double* __restrict__ B, int64_t ldb, int64_t strideB, int32_t* err_flag) {
-    const int64_t total = batch * n * nrows;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t i = e % nrows;
-        const int64_t j = (e / nrows) % n;
-        const int64_t s = e / (nrows * n);
-        const int64_t r = rows[i];
-        const bool ok = r >= 0 && r < m;  // grid.cpp:138-140 (rows beyond the matrix)
-        if (!ok && err_flag) atomicCAS(err_flag, 0, SPID_INDEX_OUT_OF_RANGE);
-        B[s * strideB + j * ldb + i] = ok ? A[s * strideA + j * lda + r] : 0.0;
+    // rows in x, (subdomain, column) pairs in y: one division per column
+    for (int64_t sj = blockIdx.y; sj < batch * n; sj += gridDim.y) {
+        const int64_t s = sj / n, j = sj - s * n;
+        const double* src = A + s * strideA + j * lda;
+        double* dst = B + s * strideB + j * ldb;
+        for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nrows;
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            const int64_t r = rows[i];
+            const bool ok = r >= 0 && r < m;  // grid.cpp:138-140 (rows beyond the matrix)
+            if (!ok && err_flag) atomicCAS(err_flag, 0, SPID_INDEX_OUT_OF_RANGE);
+            dst[i] = ok ? src[r] : 0.0;
+        }
     }
 }
 
@@ -94,11 +96,7 @@ cudaError_t launch_gather_rows(const double* A, int64_t m, int64_t n, int64_t ld
                                int64_t strideA, int64_t batch, const int64_t* rows,
                                int64_t nrows, double* B, int64_t ldb, int64_t strideB, int32_t* err_flag,
                                cudaStream_t stream) {
-    const int64_t total = batch * n * nrows;
-    int64_t grid = (total + 255) / 256;
-    if (grid > 148 * 32) grid = 148 * 32;
-    if (grid < 1) grid = 1;
-    gather_rows_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(A, m, n, lda, strideA,
+    gather_rows_kernel<<<col_grid(nrows, batch * n), 256, 0, stream>>>(A, m, n, lda, strideA,
                                                                         batch, rows, nrows, B,
                                                                         ldb, strideB, err_flag);
     return cudaGetLastError();

@@ -159,12 +159,16 @@ __global__ void gather_coarse_kernel(const double* __restrict__ A, int64_t lda, 
                                      const int64_t* __restrict__ idx, int64_t kcap,
                                      const int64_t* __restrict__ rank, int64_t batch,
                                      double* __restrict__ skel, int64_t ldskel, int64_t strideS) {
-    const int64_t total = batch * kcap * nrows;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t i = e % nrows, t = (e / nrows) % kcap, s = e / (nrows * kcap);
+    // rows in x, (subdomain, skeleton column) pairs in y; columns past the
+    // rank are skipped whole
+    for (int64_t st = blockIdx.y; st < batch * kcap; st += gridDim.y) {
+        const int64_t s = st / kcap, t = st - s * kcap;
         if (t >= rank[s]) continue;
-        skel[s * strideS + t * ldskel + i] = A[s * strideA + idx[s * kcap + t] * lda + rows[i]];
+        const double* src = A + s * strideA + idx[s * kcap + t] * lda;
+        double* dst = skel + s * strideS + t * ldskel;
+        for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nrows;
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+            dst[i] = src[rows[i]];
     }
 }
 
@@ -190,11 +194,7 @@ cudaError_t launch_gather_coarse(const double* A, int64_t lda, int64_t strideA, 
                                  int64_t nrows, const int64_t* idx, int64_t kcap,
                                  const int64_t* rank, int64_t batch, double* skel, int64_t ldskel,
                                  int64_t strideS, cudaStream_t stream) {
-    const int64_t total = batch * kcap * nrows;
-    int64_t grid = (total + 255) / 256;
-    if (grid > 148 * 16) grid = 148 * 16;
-    if (grid < 1) grid = 1;
-    gather_coarse_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(
+    gather_coarse_kernel<<<col_grid(nrows, batch * kcap), 256, 0, stream>>>(
         A, lda, strideA, rows, nrows, idx, kcap, rank, batch, skel, ldskel, strideS);
     return cudaGetLastError();
 }
