@@ -52,7 +52,10 @@ struct spidgpu_stream {
     std::string qoi, provenance;
     Layout L;
     std::vector<SGroup> groups;
-    cudaStream_t s_in = nullptr, s_cmp = nullptr;
+    // s_cmp: stage 1 of even chunks, then stage 2 and the archive; s_cmp2:
+    // stage 1 of odd chunks, so two chunks' column IDs (64 CTAs each for
+    // 64 blocks) share the GPU instead of queueing behind each other
+    cudaStream_t s_in = nullptr, s_cmp = nullptr, s_cmp2 = nullptr;
     cudaEvent_t ready = nullptr, free_ev[2] = {nullptr, nullptr};
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> s1_events;
     // event log (spid::TaskEvent): device-timeline events
@@ -63,7 +66,7 @@ struct spidgpu_stream {
     };
     std::vector<Push> pushes;
     std::vector<cudaEvent_t> closes;  // chunk c ingested (recorded before its stage 1)
-    Workspace ws_cmp, ws_fin;
+    Workspace ws_cmp, ws_cmp2, ws_fin;
     // host frames land in alternating staging buffers: the gather of one push
     // (same stream, so ordered before the buffer's next copy) overlaps the
     // next push's copy; a push returns once its own copy has read the host data
@@ -111,8 +114,10 @@ int close_chunk(spidgpu_stream* s) {
     if (cols == 0) return SPID_OK;
     const int64_t T = s->cfg.time_chunk;
     const int64_t kcap = std::min<int64_t>(s->cfg.stage1_rank, cols);
+    cudaStream_t sc = s->cur ? s->s_cmp2 : s->s_cmp;  // chunk buffer cur's stage-1 stream
+    Workspace& wsc = s->cur ? s->ws_cmp2 : s->ws_cmp;
     SCK(s, cudaEventRecord(s->ready, s->s_in));
-    SCK(s, cudaStreamWaitEvent(s->s_cmp, s->ready, 0));
+    SCK(s, cudaStreamWaitEvent(sc, s->ready, 0));
     cudaEvent_t ce;
     SCK(s, cudaEventCreate(&ce));
     SCK(s, cudaEventRecord(ce, s->s_in));
@@ -120,7 +125,7 @@ int close_chunk(spidgpu_stream* s) {
     cudaEvent_t e0, e1;
     SCK(s, cudaEventCreate(&e0));
     SCK(s, cudaEventCreate(&e1));
-    SCK(s, cudaEventRecord(e0, s->s_cmp));
+    SCK(s, cudaEventRecord(e0, sc));
     spidgpu_rank_rule rule{SPIDGPU_RULE_FIXED, 1, kcap, 0, 0.0};  // column_id_at_most(chunk, min(k, cols))
     for (SGroup& g : s->groups) {
         ChunkArena c;
@@ -136,24 +141,24 @@ int close_chunk(spidgpu_stream* s) {
         c.o_sidx = cv.take<int64_t>(g.nb * kcap);
         c.o_spos = cv.take<int32_t>(g.nb * kcap);
         c.o_skel = cv.take<double>(g.nb * kcap * g.Pc);
-        SCK(s, cudaMallocAsync(&c.mem, cv.off, s->s_cmp));
+        SCK(s, cudaMallocAsync(&c.mem, cv.off, sc));
         const double* chunk = g.chunkbuf[s->cur].as<double>();
-        SRC(s, do_cpqr(s->h, s->ws_cmp, chunk, g.Pc, cols, g.Pc, g.Pc * T, g.nb, &rule, kcap,
+        SRC(s, do_cpqr(s->h, wsc, chunk, g.Pc, cols, g.Pc, g.Pc * T, g.nb, &rule, kcap,
                        c.p<int64_t>(c.o_idx), c.p<double>(c.o_C0), kcap * cols, c.p<int64_t>(c.o_rank),
-                       c.p<double>(c.o_resid), c.p<int32_t>(c.o_status), nullptr, nullptr, nullptr, s->s_cmp));
+                       c.p<double>(c.o_resid), c.p<int32_t>(c.o_status), nullptr, nullptr, nullptr, sc));
         // skeleton = the chunk's coarse columns, kept in sorted (union) order
         SCK(s, launch_sort_pairs(c.p<int64_t>(c.o_idx), c.p<int64_t>(c.o_rank), kcap, g.nb,
-                                 c.p<int64_t>(c.o_sidx), c.p<int32_t>(c.o_spos), s->s_cmp));
+                                 c.p<int64_t>(c.o_sidx), c.p<int32_t>(c.o_spos), sc));
         SCK(s, launch_gather_cols(chunk, g.Pc, g.Pc, g.Pc * T, g.nb, c.p<int64_t>(c.o_sidx), kcap,
                                   c.p<int64_t>(c.o_rank), cols, c.p<double>(c.o_skel), g.Pc, g.Pc * kcap,
-                                  nullptr, s->s_cmp));
+                                  nullptr, sc));
         s->h->launches += 2;
         g.used[s->cur] = true;
         g.chunks.push_back(c);
         s->stage1_tasks += g.nb;
     }
-    SCK(s, cudaEventRecord(e1, s->s_cmp));
-    SCK(s, cudaEventRecord(s->free_ev[s->cur], s->s_cmp));
+    SCK(s, cudaEventRecord(e1, sc));
+    SCK(s, cudaEventRecord(s->free_ev[s->cur], sc));
     s->s1_events.emplace_back(e0, e1);
     s->cur ^= 1;
     s->filled = 0;
@@ -181,6 +186,7 @@ struct Stream_push_log {
 
 void destroy(spidgpu_stream* s) {
     if (s->s_cmp) cudaStreamSynchronize(s->s_cmp);
+    if (s->s_cmp2) cudaStreamSynchronize(s->s_cmp2);
     if (s->s_in) cudaStreamSynchronize(s->s_in);
     for (SGroup& g : s->groups) {
         for (ChunkArena& c : g.chunks)
@@ -192,6 +198,7 @@ void destroy(spidgpu_stream* s) {
         g.fin.release();
     }
     s->ws_cmp.release();
+    s->ws_cmp2.release();
     s->ws_fin.release();
     s->staging[0].release();
     s->staging[1].release();
@@ -212,6 +219,7 @@ void destroy(spidgpu_stream* s) {
         if (e) cudaEventDestroy(e);
     if (s->s_in) cudaStreamDestroy(s->s_in);
     if (s->s_cmp) cudaStreamDestroy(s->s_cmp);
+    if (s->s_cmp2) cudaStreamDestroy(s->s_cmp2);
 }
 
 }  // namespace
@@ -255,6 +263,7 @@ int spidgpu_stream_open(spidgpu_handle h, const spidgpu_stream_config* cfg, spid
     };
     if (cudaStreamCreateWithFlags(&s->s_in, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&s->s_cmp, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&s->s_cmp2, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&s->ready, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&s->free_ev[0], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&s->free_ev[1], cudaEventDisableTiming) != cudaSuccess ||
@@ -345,6 +354,7 @@ int spidgpu_stream_finish(spidgpu_stream_handle s, int64_t* nbytes) {
     if (rc) return rc;
     if (s->snapshots == 0) return sfail(s, SPID_SHORT_STREAM, "producer yielded no snapshots");
     SCK(s, cudaStreamSynchronize(s->s_cmp));
+    SCK(s, cudaStreamSynchronize(s->s_cmp2));
     s->finished = true;
     const int64_t nblocks = static_cast<int64_t>(s->L.doms.size());
     const int64_t n_total = s->snapshots, T = s->cfg.time_chunk;
