@@ -628,7 +628,7 @@ def e2e_measure(eng, cfg, A, first, count, rule, args, world):
             "residual_fro": torch.empty(ne, dtype=torch.float64, pin_memory=True),
             "status": torch.empty(ne, dtype=torch.int32, pin_memory=True),
         }
-        eng.compress_host(a_host, cfg.ell, rule, seed=cfg.seed, subdomain_base=first, group=8,
+        eng.compress_host(a_host, cfg.ell, rule, seed=cfg.seed, subdomain_base=first, group=2,
                           out=out)  # warm-up (allocates the lane buffers)
         torch.cuda.synchronize()
     except Exception as e:  # host memory / pinning failure: reported, never fatal
@@ -642,7 +642,7 @@ def e2e_measure(eng, cfg, A, first, count, rule, args, world):
         dist.barrier()
     t = time.perf_counter()
     for _ in range(args.e2e_steps):
-        eng.compress_host(a_host, cfg.ell, rule, seed=cfg.seed, subdomain_base=first, group=8,
+        eng.compress_host(a_host, cfg.ell, rule, seed=cfg.seed, subdomain_base=first, group=2,
                           out=out)
     el = torch.tensor([(time.perf_counter() - t) / args.e2e_steps], dtype=torch.float64,
                       device=eng.dev)
