@@ -389,6 +389,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t c = blockIdx.x;
     const uint32_t rank = kPair ? cluster_ctarank() : 0u;
+    // the peer's shared::cluster window is this CTA's layout shifted by a
+    // constant: remote = local + poff (one mapa instead of one per store)
+    const uint32_t poff = kPair ? peer_addr(base_s, rank ^ 1u) - base_s : 0u;
     const int64_t G = gridDim.x / P, cu = c / P;  // work-unit owners: CTAs, or CTA pairs
     const int64_t lo = sketch_unit_chunk((cu * total_units) / G, nseg, seg_len, nchunk);
     const int64_t hi = sketch_unit_chunk(((cu + 1) * total_units) / G, nseg, seg_len, nchunk);
@@ -443,7 +446,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr uint32_t kPeerBytes = kTasksCta * (kFine ? 8 : 16);  // Omega bytes the peer sends per stage
         static_assert(kTasksPerWarp <= 32, "one Omega task per lane");
         const int gw = warp == 0 ? 0 : warp - 1;
-        const uint32_t peer = rank ^ 1u;
 
         constexpr uint32_t kIdU = idesc_i8(NPAD, false);
         const uint64_t ones_desc = smem_desc(ones_s, 0, 0);
@@ -548,7 +550,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 else
                     sts128u(dst, w[0], w[1], w[2 * kOct - 2], w[2 * kOct - 1]);
                 if constexpr (kPair) {  // the peer's copy, counted on its stage barrier
-                    const uint32_t rdst = peer_addr(dst, peer), rbar = peer_addr(smem_u32(&b_full[sl]), peer);
+                    const uint32_t rdst = dst + poff, rbar = smem_u32(&b_full[sl]) + poff;
                     if constexpr (kFine)
                         st_async_v2(rdst, w[0], w[1], rbar);
                     else
@@ -646,8 +648,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if constexpr (kSplit) {
                 if (b == 0) {
                     const int sa = it % kAStages;
-                    st_async_b32(peer_addr(mbox_s + (sa * kM + col) * 4, rank ^ 1u), mx,
-                                 peer_addr(smem_u32(&m_full[sa]), rank ^ 1u));
+                    st_async_b32(mbox_s + (sa * kM + col) * 4 + poff, mx, smem_u32(&m_full[sa]) + poff);
                 }
             }
             __syncwarp();
@@ -763,22 +764,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // CTA 0 keeps slices 0-3 (tiles 0-3), CTA 1 slices 4-6 (tiles
                     // 0-2); the other CTA's slices go to its tiles at the same
                     // offset, counted on its stage barrier
-                    const uint32_t peer = rank ^ 1u;
-                    const uint32_t rbar = peer_addr(smem_u32(&b_full[sb]), peer);
+                    const uint32_t rbar = smem_u32(&b_full[sb]) + poff;
                     if (rank == 0) {
 #pragma unroll
                         for (int t = 0; t < 4; ++t) sts128u(st + t * kTileBytes, sw[t][0], sw[t][1], sw[t][2], sw[t][3]);
 #pragma unroll
                         for (int t = 4; t < kSlices; ++t)
-                            st_async_v4(peer_addr(st + (t - 4) * kTileBytes, peer), sw[t][0], sw[t][1], sw[t][2], sw[t][3],
-                                        rbar);
+                            st_async_v4(st + (t - 4) * kTileBytes + poff, sw[t][0], sw[t][1], sw[t][2], sw[t][3], rbar);
                     } else {
 #pragma unroll
                         for (int t = 4; t < kSlices; ++t)
                             sts128u(st + (t - 4) * kTileBytes, sw[t][0], sw[t][1], sw[t][2], sw[t][3]);
 #pragma unroll
                         for (int t = 0; t < 4; ++t)
-                            st_async_v4(peer_addr(st + t * kTileBytes, peer), sw[t][0], sw[t][1], sw[t][2], sw[t][3], rbar);
+                            st_async_v4(st + t * kTileBytes + poff, sw[t][0], sw[t][1], sw[t][2], sw[t][3], rbar);
                     }
                 }
             };
