@@ -329,8 +329,14 @@ __global__ void __launch_bounds__(kReconThreads, SPIDGPU_RECON_MINB)
             double acc0[kReconNJ], acc1[kReconNJ];
 #pragma unroll
             for (int u = 0; u < kReconNJ; ++u) acc0[u] = acc1[u] = 0.0;
+            // F(i, t) of the next t is loaded while this t's products run
+            double a0n = k > 0 ? __ldg(fp0) : 0.0, a1n = k > 0 ? __ldg(fp1) : 0.0;
             for (int t = 0; t < k; ++t) {
-                const double a0 = __ldg(fp0 + t * ldf), a1 = __ldg(fp1 + t * ldf);
+                const double a0 = a0n, a1 = a1n;
+                if (t + 1 < k) {
+                    a0n = __ldg(fp0 + (t + 1) * ldf);
+                    a1n = __ldg(fp1 + (t + 1) * ldf);
+                }
                 const double* ct = cs + t * kReconCols + j0;
                 const uint32_t nz = static_cast<uint32_t>(nzm[t] >> j0) & 0xffffu;
                 if (nz == 0xffffu) {
