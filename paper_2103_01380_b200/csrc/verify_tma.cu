@@ -221,16 +221,27 @@ __global__ void __launch_bounds__(kThreadsV, 1)
 // err2[s], ref2[s]: fixed-order sum over the subdomain's column tiles,
 // their segments and the warps' partials.
 __global__ void verify_tma_finish(VerifyParams p, int64_t ntiles_col, int64_t nseg, const double* part) {
-    const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    // one warp per subdomain: lane l adds partials l, l + 32, ... in order,
+    // then a fixed butterfly -- a fixed association per subdomain, so the
+    // sums stay independent of the batch
+    const int64_t s = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (s >= p.batch) return;
     double e = 0.0, r = 0.0;
     const double* src = part + static_cast<size_t>(s) * ntiles_col * nseg * kCons * 2;
-    for (int64_t g = 0; g < ntiles_col * nseg * kCons; ++g) {
+    for (int64_t g = lane; g < ntiles_col * nseg * kCons; g += 32) {
         e += src[2 * g];
         r += src[2 * g + 1];
     }
-    p.err2[s] = e;
-    p.ref2[s] = r;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        e += __shfl_xor_sync(0xffffffffu, e, off);
+        r += __shfl_xor_sync(0xffffffffu, r, off);
+    }
+    if (lane == 0) {
+        p.err2[s] = e;
+        p.ref2[s] = r;
+    }
 }
 
 template <int NWV, int KS>
@@ -245,8 +256,8 @@ cudaError_t launch_t(const VerifyParams& p, const VerifyPlan& plan, const CUtens
                                                        plan.seg_len, plan.total_units, part);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    verify_tma_finish<<<static_cast<unsigned>((p.batch + 127) / 128), 128, 0, stream>>>(p, plan.ntiles_col,
-                                                                                         plan.nseg, part);
+    verify_tma_finish<<<static_cast<unsigned>((p.batch + 3) / 4), 128, 0, stream>>>(p, plan.ntiles_col, plan.nseg,
+                                                                                     part);
     return cudaGetLastError();
 }
 
