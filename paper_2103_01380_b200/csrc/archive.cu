@@ -227,23 +227,43 @@ __global__ void __launch_bounds__(kCrcThreads)
     }
 }
 
-// One thread per section: fold its parts (all but the first are kCrcPart
-// long), condition, optionally write the 4 CRC bytes after the payload.
+// One block per section: part q's raw CRC shifted past the (full) parts after
+// it, x^(8 kCrcPart (last - q)) * crc_q, XOR-reduced -- the same GF(2) sum the
+// sequential fold acc = x^(8 kCrcPart) acc ^ crc_q forms, so the same bits;
+// then conditioned, optionally written after the payload.
 __global__ void crc_fold_kernel(const CrcSection* __restrict__ secs, int64_t nsec,
                                 const int64_t* __restrict__ first_part, const uint32_t* __restrict__ part_crc,
                                 uint32_t* __restrict__ crc_out, uint8_t* write_back) {
-    const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    __shared__ uint32_t wred[32];
+    const int64_t s = blockIdx.x;
     if (s >= nsec) return;
     const uint32_t xpart = xpow8_d(static_cast<uint64_t>(kCrcPart));
+    const int64_t f = first_part[s], l = first_part[s + 1];
     uint32_t acc = 0;
-    for (int64_t q = first_part[s]; q < first_part[s + 1]; ++q) acc = multmodp_d(xpart, acc) ^ part_crc[q];
-    const int64_t len = secs[s].len;
-    const uint32_t crc = ~(acc ^ multmodp_d(xpow8_d(static_cast<uint64_t>(len)), 0xFFFFFFFFu));
-    crc_out[s] = crc;
-    if (write_back) {
-        const int64_t end = secs[s].begin + len;
+    for (int64_t q = f + threadIdx.x; q < l; q += blockDim.x) {
+        uint32_t pw = 1u << 31, sq = xpart;  // xpart^(l - 1 - q)
+        for (uint64_t e = static_cast<uint64_t>(l - 1 - q); e; e >>= 1) {
+            if (e & 1) pw = multmodp_d(sq, pw);
+            sq = multmodp_d(sq, sq);
+        }
+        acc ^= multmodp_d(pw, part_crc[q]);
+    }
 #pragma unroll
-        for (int b = 0; b < 4; ++b) write_back[end + b] = static_cast<uint8_t>(crc >> (8 * b));
+    for (int off = 16; off > 0; off >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, off);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) wred[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        acc = 0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) acc ^= wred[w];
+        const int64_t len = secs[s].len;
+        const uint32_t crc = ~(acc ^ multmodp_d(xpow8_d(static_cast<uint64_t>(len)), 0xFFFFFFFFu));
+        crc_out[s] = crc;
+        if (write_back) {
+            const int64_t end = secs[s].begin + len;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) write_back[end + b] = static_cast<uint8_t>(crc >> (8 * b));
+        }
     }
 }
 
@@ -471,8 +491,8 @@ cudaError_t launch_crc_sections(const uint8_t* data, const CrcSection* secs, int
                                                                                  part_crc);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    crc_fold_kernel<<<static_cast<unsigned>((nsec + 127) / 128), 128, 0, st>>>(secs, nsec, first_part, part_crc,
-                                                                               crc_out, write_back);
+    crc_fold_kernel<<<static_cast<unsigned>(nsec < 1 ? 1 : nsec), 256, 0, st>>>(secs, nsec, first_part, part_crc,
+                                                                                crc_out, write_back);
     return cudaGetLastError();
 }
 
