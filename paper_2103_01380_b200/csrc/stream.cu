@@ -43,26 +43,42 @@ __global__ void sort_pairs_kernel(const int64_t* __restrict__ idx, const int64_t
     }
 }
 
+// Per block b: the chunks' skeleton columns back to back (the union in
+// chunk order), their global indices and stage-1 positions, and the chunk
+// offsets. Grid (x, b): CTA x == 0 writes the bookkeeping; every CTA copies a
+// grid-strided share of each chunk's contiguous r x mc range (16-byte
+// vectors when mc is even), so the copy is spread over ~8 CTAs per SM.
 __global__ void concat_union_kernel(const StreamChunkDev* __restrict__ chunks, int64_t nchunks,
                                     int64_t mc, int64_t rmax, double* __restrict__ concat,
                                     int64_t* __restrict__ uglob, int32_t* __restrict__ upos,
                                     int64_t* __restrict__ uoff, int64_t* __restrict__ R) {
-    const int64_t b = blockIdx.x;
+    const int64_t b = blockIdx.y;
     double* cb = concat + b * rmax * mc;
+    const int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     int64_t u0 = 0;
     for (int64_t c = 0; c < nchunks; ++c) {
         const StreamChunkDev ch = chunks[c];
         const int64_t r = ch.rank[b];
-        if (threadIdx.x == 0) uoff[b * (nchunks + 1) + c] = u0;
-        for (int64_t u = threadIdx.x; u < r; u += blockDim.x) {
-            uglob[b * rmax + u0 + u] = ch.col0 + ch.sorted_idx[b * ch.kcap + u];
-            upos[b * rmax + u0 + u] = ch.sorted_pos[b * ch.kcap + u];
+        if (blockIdx.x == 0) {
+            if (threadIdx.x == 0) uoff[b * (nchunks + 1) + c] = u0;
+            for (int64_t u = threadIdx.x; u < r; u += blockDim.x) {
+                uglob[b * rmax + u0 + u] = ch.col0 + ch.sorted_idx[b * ch.kcap + u];
+                upos[b * rmax + u0 + u] = ch.sorted_pos[b * ch.kcap + u];
+            }
         }
         const double* src = ch.skel + b * ch.kcap * mc;
-        for (int64_t e = threadIdx.x; e < r * mc; e += blockDim.x) cb[u0 * mc + e] = src[e];
+        double* dst = cb + u0 * mc;
+        if ((mc & 1) == 0) {
+            const double2* s2 = reinterpret_cast<const double2*>(src);
+            double2* d2 = reinterpret_cast<double2*>(dst);
+            for (int64_t e = t0; e < r * mc / 2; e += stride) d2[e] = s2[e];
+        } else {
+            for (int64_t e = t0; e < r * mc; e += stride) dst[e] = src[e];
+        }
         u0 += r;
     }
-    if (threadIdx.x == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
         uoff[b * (nchunks + 1) + nchunks] = u0;
         R[b] = u0;
     }
@@ -117,8 +133,11 @@ cudaError_t launch_sort_pairs(const int64_t* idx, const int64_t* rank, int64_t k
 cudaError_t launch_concat_union(const StreamChunkDev* chunks, int64_t nchunks, int64_t nb, int64_t mc,
                                 int64_t rmax, double* concat, int64_t* uglob, int32_t* upos,
                                 int64_t* uoff, int64_t* R, cudaStream_t st) {
-    concat_union_kernel<<<static_cast<unsigned>(nb), 256, 0, st>>>(chunks, nchunks, mc, rmax, concat, uglob,
-                                                                    upos, uoff, R);
+    int64_t gx = (148 * 8 + nb - 1) / nb;
+    if (gx > 64) gx = 64;
+    if (gx < 1) gx = 1;
+    concat_union_kernel<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(nb)), 256, 0, st>>>(
+        chunks, nchunks, mc, rmax, concat, uglob, upos, uoff, R);
     return cudaGetLastError();
 }
 
