@@ -108,6 +108,11 @@ int64_t spidgpu_launch_count(spidgpu_handle h);
 #define SPIDGPU_OPT_SKETCH_SMS 4
 #define SPIDGPU_OPT_SKETCH_PAIRS 5
 #define SPIDGPU_OPT_SKETCH_SEG_ROWS 6
+/* SPIDGPU_OPT_TALL_PAIRS = 7: tall column IDs (rows >= 256) with 64 < n <= 256
+ * columns and the fixed or tolerance rule run each subdomain's columns on a
+ * cluster of two CTAs (1, default) or on one CTA (0); bitwise the same
+ * factors (tests and A/B). */
+#define SPIDGPU_OPT_TALL_PAIRS 7
 int spidgpu_set_option(spidgpu_handle h, int option, int64_t value);
 /* Instrumentation: out[0..2] = tcgen05-sketch converter-warp flushes since
  * the last reset, by cause (segment end, exponent-headroom overflow,

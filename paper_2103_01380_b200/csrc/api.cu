@@ -180,11 +180,13 @@ int do_cpqr(spidgpu_handle h, Workspace& ws, const double* Y, int64_t rows, int6
     const bool w_smem = cpqr_smem_bytes(rows, n, step_cap, true) <= cpqr_max_dyn_smem();
     // W too large for shared memory: tall inputs stream it through a TMA ring
     const bool tall = !reg && !w_smem && cpqr_tall_supported(rows, n);
-    const int npad = tall ? cpqr_tall_npad(n) : static_cast<int>(n);
+    // wide tall inputs: each subdomain's columns over a cluster of two
+    const bool pair = tall && h->tall_pairs && cpqr_pair_supported(rows, n, rule->mode, step_cap);
+    const int npad = pair ? 2 * cpqr_pair_half(n) : tall ? cpqr_tall_npad(n) : static_cast<int>(n);
     CK(h, ws.rws.ensure(sizeof(double) * batch * step_cap * n, st));
     if (!reg && !w_smem) {
         CK(h, ws.wws.ensure(sizeof(double) * batch * rows * npad, st));
-        CK(h, ws.r11ws.ensure(sizeof(double) * batch * step_cap * step_cap, st));
+        CK(h, ws.r11ws.ensure(sizeof(double) * batch * (pair ? 2 : 1) * step_cap * step_cap, st));
     }
     CpqrParams p{};
     p.Y = Y;
@@ -221,14 +223,15 @@ int do_cpqr(spidgpu_handle h, Workspace& ws, const double* Y, int64_t rows, int6
         cuuint64_t gdim[3] = {static_cast<cuuint64_t>(npad), static_cast<cuuint64_t>(rows),
                               static_cast<cuuint64_t>(batch)};
         cuuint64_t gstride[2] = {static_cast<cuuint64_t>(npad) * 8, static_cast<cuuint64_t>(rows) * npad * 8};
-        cuuint32_t box[3] = {static_cast<cuuint32_t>(npad), static_cast<cuuint32_t>(cpqr_tall_ring_rows(n)), 1};
+        cuuint32_t box[3] = {static_cast<cuuint32_t>(pair ? cpqr_pair_half(n) : npad),
+                             static_cast<cuuint32_t>(pair ? cpqr_pair_ring_rows(n) : cpqr_tall_ring_rows(n)), 1};
         cuuint32_t estr[3] = {1, 1, 1};
         CUresult cr = h->encode(&wmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, ws.wws.ptr, gdim, gstride, box, estr,
                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (cr != CUDA_SUCCESS)
             return fail(h, SPID_SHAPE_UNSUPPORTED, "cuTensorMapEncodeTiled (CPQR ring) failed: " + std::to_string(cr));
-        CK(h, launch_cpqr_tall(p, &wmap, st));
+        CK(h, pair ? launch_cpqr_pair(p, &wmap, st) : launch_cpqr_tall(p, &wmap, st));
     } else {
         CK(h, launch_cpqr(p, w_smem, st));
     }
@@ -606,6 +609,7 @@ int spidgpu_set_option(spidgpu_handle h, int option, int64_t value) {
     if (!h) return SPID_INVALID_ARGUMENT;
     switch (option) {
         case SPIDGPU_OPT_GENERIC_CPQR: h->force_generic_cpqr = value != 0; return SPID_OK;
+        case SPIDGPU_OPT_TALL_PAIRS: h->tall_pairs = value != 0; return SPID_OK;
         case SPIDGPU_OPT_DMMA_SKETCH: h->force_dmma_sketch = value != 0; return SPID_OK;
         case SPIDGPU_OPT_SKETCH_PAIRS:
             if (value < 0 || value > 2) return SPID_INVALID_ARGUMENT;

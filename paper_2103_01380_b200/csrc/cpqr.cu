@@ -384,7 +384,21 @@ __global__ void __launch_bounds__(kMode == 2 ? kCpqrThreads + kWarp : kCpqrThrea
         const int pc = sh.best_i;
         const double pn = sh.best_v;
         // q_s = w_s / R(s,s) (qr.cpp:91-92)
-        for (int i = tid; i < rows; i += kCpqrThreads) W[i * npad + pc] = div_rn(W[i * npad + pc], pn);
+        // (the column's strided loads issued 8 per thread at a time, then
+        // divided and stored)
+        for (int i0 = 0; i0 < rows; i0 += 8 * kCpqrThreads) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * kCpqrThreads + tid;
+                v[u] = i < rows ? W[i * npad + pc] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * kCpqrThreads + tid;
+                if (i < rows) W[i * npad + pc] = div_rn(v[u], pn);
+            }
+        }
         if constexpr (kMode == 2) {
             // two-pass MGS (qr.cpp:94-102) over the TMA ring, as three read
             // sweeps of the step's W that stream back to back (nothing is

@@ -108,3 +108,55 @@ def test_tall_batched_statuses_and_parity(engine, orc):
         assert np.array_equal(res.indices[s].cpu().numpy(), o.indices)
         assert np.array_equal(np.asfortranarray(res.coeffs[s].cpu().numpy().T), o.coeffs)
         assert float(res.residual_fro[s]) == o.residual_fro
+
+
+@pytest.fixture(params=[1, 0], ids=["pairs", "single"])
+def tall_pairs(request, spid):
+    """Wide tall inputs (64 < n <= 256, fixed / tolerance rules) run on a
+    cluster of two CTAs by default (cpqr_pair.cu); 0 forces one CTA."""
+    from paper_2103_01380_b200 import _native as N
+
+    h = spid._h(0)
+    h.check(N.lib.spidgpu_set_option(h.h, N.SPIDGPU_OPT_TALL_PAIRS, request.param))
+    yield request.param
+    h.check(N.lib.spidgpu_set_option(h.h, N.SPIDGPU_OPT_TALL_PAIRS, 1))
+
+
+@pytest.mark.parametrize("m,n,k", [(4096, 256, 32), (1000, 200, 24), (2500, 130, 40), (3000, 100, 20),
+                                   (257, 255, 60), (600, 65, 65)])
+def test_tall_pairs_bitwise(tall_pairs, spid, orc, m, n, k):
+    """The pair kernel and the single-CTA kernel both equal the oracle bit for
+    bit: pivots, coefficients, residual, and Q / R."""
+    a = orc.seeded_matrix(m, n, 17 + m + n)
+    g = spid.column_id(a, rank=k)
+    o = orc.column_id(a, rank=k)
+    assert g.achieved_rank == o.rank == k
+    assert _eq(g.skeleton_indices, o.indices) and _eq(g.coeffs, o.coeffs)
+    assert g.qr_residual_fro == o.residual_fro
+    q = spid.qr(a, rank=min(k, 12))
+    qo = orc.qr(a, rank=min(k, 12))
+    assert _eq(q["q"], qo.q) and _eq(q["r"], qo.r) and _eq(q["pivots"], qo.pivots)
+
+
+@pytest.mark.parametrize("tol", [1e-1, 1e-6])
+def test_tall_pairs_tolerance_and_errors(tall_pairs, spid, orc, tol):
+    """Tolerance rule and the error exits through the pair (the peer must
+    never be left waiting): rank-deficient input with a strict fixed rank,
+    and a non-finite entry in the second CTA's half."""
+    from paper_2103_01380_b200 import SpidError
+
+    a = orc.seeded_matrix(3000, 180, 7)
+    g = spid.column_id(a, tol=tol)
+    o = orc.column_id(a, tol=tol)
+    assert g.achieved_rank == o.rank and _eq(g.skeleton_indices, o.indices) and _eq(g.coeffs, o.coeffs)
+    low = np.asfortranarray(orc.seeded_matrix(3000, 5, 8) @ orc.seeded_matrix(5, 180, 9))
+    with pytest.raises(SpidError) as e:
+        spid.column_id(low, rank=40)
+    assert e.value.name == "RankUnreachable"
+    bad = a.copy()
+    bad[1234, 170] = np.nan
+    with pytest.raises(SpidError) as e:
+        spid.column_id(bad, rank=10)
+    assert e.value.name == "NonFiniteInput"
+    # the handle still works afterwards
+    assert spid.column_id(a, rank=10).achieved_rank == 10
