@@ -13,8 +13,9 @@
 //     peer's slot, completing on its mbarrier) and pick the same winner (the
 //     total order of qr.cpp:68);
 //   - share the normalised pivot column q: its owner writes it into its own
-//     shared memory and, by st.async, into the peer's before the sweeps,
-//     which read q from there instead of from the ring chunk;
+//     shared memory and, by distributed-shared stores, into the peer's, then
+//     releases it with one cluster-scope arrive on the peer's q barrier; the
+//     sweeps read q from there instead of from the ring chunk;
 //   - keep identical copies of the position bookkeeping (perm / posof).
 // The producer warps keep streaming while the column warps trade, so the
 // pair meets at a cluster barrier only at the start and once at the end,
@@ -341,7 +342,10 @@ __global__ void __launch_bounds__(kThr + kWarp, 1)
             if (tid == 0) {
                 const double pv = __hiloint2double(static_cast<int>(x.w[1]), static_cast<int>(x.w[0]));
                 const int pi = static_cast<int>(x.w[2]);
-                if (key_better(pv, pi, lv, li)) {
+                // the same comparison, operands in rank order, in both CTAs:
+                // they agree on the pivot even when a norm is NaN
+                const bool peer_wins = crank == 0 ? key_better(pv, pi, lv, li) : !key_better(lv, li, pv, pi);
+                if (peer_wins) {
                     sh.best_v = pv;
                     sh.best_i = pi;
                 }
@@ -383,8 +387,8 @@ __global__ void __launch_bounds__(kThr + kWarp, 1)
         // peer finished the previous step's sweeps before it sent this step's
         // argmax, so its q is free.
         if (pc >= c0 && pc < c1) {
-            // the column's strided global loads issued together, 8 per thread
-            // at a time, then divided and stored
+            // the column's strided global loads issued together, 16 per
+            // thread at a time, then divided and stored
             for (int i0 = 0; i0 < rows; i0 += 16 * kThr) {
                 double v[16];
 #pragma unroll
