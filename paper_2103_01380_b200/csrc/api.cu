@@ -231,7 +231,17 @@ int do_cpqr(spidgpu_handle h, Workspace& ws, const double* Y, int64_t rows, int6
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (cr != CUDA_SUCCESS)
             return fail(h, SPID_SHAPE_UNSUPPORTED, "cuTensorMapEncodeTiled (CPQR ring) failed: " + std::to_string(cr));
-        CK(h, pair ? launch_cpqr_pair(p, &wmap, st) : launch_cpqr_tall(p, &wmap, st));
+        CUtensorMap pmap;  // pairs: the pivot column pair beside each first-sweep chunk
+        if (pair) {
+            cuuint32_t pbox[3] = {2, box[1], 1};
+            cr = h->encode(&pmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, ws.wws.ptr, gdim, gstride, pbox, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (cr != CUDA_SUCCESS)
+                return fail(h, SPID_SHAPE_UNSUPPORTED, "cuTensorMapEncodeTiled (CPQR pivot column) failed: " +
+                                                           std::to_string(cr));
+        }
+        CK(h, pair ? launch_cpqr_pair(p, &wmap, &pmap, st) : launch_cpqr_tall(p, &wmap, st));
     } else {
         CK(h, launch_cpqr(p, w_smem, st));
     }

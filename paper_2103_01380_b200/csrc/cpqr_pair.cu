@@ -12,10 +12,10 @@
 //   - trade their local (norm, index) maxima (16-byte st.async into the
 //     peer's slot, completing on its mbarrier) and pick the same winner (the
 //     total order of qr.cpp:68);
-//   - share the normalised pivot column q: its owner writes it into its own
-//     shared memory and, by distributed-shared stores, into the peer's, then
-//     releases it with one cluster-scope arrive on the peer's q barrier; the
-//     sweeps read q from there instead of from the ring chunk;
+//   - both compute the normalised pivot column q themselves: the producer
+//     loads the pivot column pair beside every first-sweep chunk (a second
+//     tensor map, box {2, ring_rows}) and an idle warp divides it into qsm
+//     with the same rounding, ahead of the column warps;
 //   - keep identical copies of the position bookkeeping (perm / posof).
 // The producer warps keep streaming while the column warps trade, so the
 // pair meets at a cluster barrier only at the start and once at the end,
@@ -93,25 +93,28 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase)
 
 struct PairShared {
     double best_v, max_init;
-    int best_i, stop, flag, chunks;
+    int best_i, stop, flag, chunks, side_pc;
 };
 // A point-to-point exchange slot: 16 bytes the peer writes by st.async
 struct alignas(16) XSlot {
     uint32_t w[4];
 };
 constexpr int kXSlots = 4;
+constexpr int kQWarp = kThr / kWarp - 1;  // idle column warp (NH <= 128): computes q
 
 // NH: columns per CTA (half of the padded row length); W rows are 2 NH long.
 template <int NH>
 __global__ void __launch_bounds__(kThr + kWarp, 1)
-    cpqr_pair_kernel(CpqrParams p, const __grid_constant__ CUtensorMap wmap, int ring_rows) {
+    cpqr_pair_kernel(CpqrParams p, const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap pmap,
+                     int ring_rows) {
     constexpr int npad = 2 * NH;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ PairShared sh;
     __shared__ double red_v[kThr / kWarp];
     __shared__ int red_i[kThr / kWarp];
     __shared__ uint64_t ring_full[kStages], ring_empty[kStages], go_bar;
-    __shared__ uint64_t xbar[kXSlots], qbar;  // exchanges with the peer; its pivot column
+    __shared__ uint64_t xbar[kXSlots];  // exchanges with the peer
+    __shared__ uint64_t qready[kStages];  // q of a first-sweep chunk is in qsm
     __shared__ XSlot xs[kXSlots];
 
     const uint32_t crank = ctarank(), peer = crank ^ 1u;
@@ -122,10 +125,12 @@ __global__ void __launch_bounds__(kThr + kWarp, 1)
     const int j = c0 + tid;                       // this thread's column
     const bool mine = tid < NH && j < c1;
 
-    // smem: ring | q[rows] | nrm[n] perm[n] posof[n] | diag[cap]
+    // smem: ring | side ring | q[rows] | nrm[n] perm[n] posof[n] | diag[cap]
     unsigned char* cur = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     double* ring = reinterpret_cast<double*>(cur);
     cur += static_cast<size_t>(kStages) * kStageBytes;
+    double* side = reinterpret_cast<double*>(cur);  // per stage: the pivot column pair, ring_rows x 2
+    cur += static_cast<size_t>(kStages) * ring_rows * 2 * sizeof(double);
     double* qsm = reinterpret_cast<double*>(cur);
     cur += sizeof(double) * ((rows + 1) & ~1);
     double* nrm = reinterpret_cast<double*>(cur);
@@ -149,7 +154,7 @@ __global__ void __launch_bounds__(kThr + kWarp, 1)
         }
         mbar_init(&go_bar, 1);
         for (int i = 0; i < kXSlots; ++i) mbar_init(&xbar[i], 1);
-        mbar_init(&qbar, 1);
+        for (int i = 0; i < kStages; ++i) mbar_init(&qready[i], 1);
         fence_barrier_init();
     }
     __syncthreads();
@@ -158,19 +163,25 @@ __global__ void __launch_bounds__(kThr + kWarp, 1)
     if (warp == kProducer) {
         if (lane == 0) {
             prefetch_tmap(&wmap);
+            prefetch_tmap(&pmap);
             const uint32_t bytes = static_cast<uint32_t>(ring_rows) * NH * sizeof(double);
+            const uint32_t sbytes = static_cast<uint32_t>(ring_rows) * 2 * sizeof(double);
             uint32_t g = 0, gophase = 0;
             for (;;) {
                 mbar_wait(&go_bar, gophase);
                 gophase ^= 1;
-                const int chunks = sh.chunks;
+                const int chunks = sh.chunks, spc = sh.side_pc;
                 if (chunks == 0) break;
                 for (int c = 0; c < chunks; ++c, ++g) {
                     const uint32_t slot = g % kStages;
+                    const bool sd = spc >= 0 && c < nck;  // first sweep of a step: the pivot column too
                     if (g >= kStages) mbar_wait(&ring_empty[slot], ((g / kStages) - 1) & 1);
-                    mbar_arrive_expect_tx(&ring_full[slot], bytes);
+                    mbar_arrive_expect_tx(&ring_full[slot], bytes + (sd ? sbytes : 0u));
                     tma_load_3d(ring + static_cast<size_t>(slot) * (kStageBytes / sizeof(double)), &wmap,
                                 &ring_full[slot], c0, (c % nck) * ring_rows, b);
+                    if (sd)
+                        tma_load_3d(side + static_cast<size_t>(slot) * ring_rows * 2, &pmap, &ring_full[slot],
+                                    spc & ~1, (c % nck) * ring_rows, b);
                 }
             }
         }
@@ -180,7 +191,7 @@ __global__ void __launch_bounds__(kThr + kWarp, 1)
     }
 
     const uint32_t poff = mapa(smem_u32(&sh), peer) - smem_u32(&sh);  // peer window = local + poff
-    const uint32_t peer_q = smem_u32(qsm) + poff, peer_nrm = smem_u32(nrm) + poff;
+    const uint32_t peer_nrm = smem_u32(nrm) + poff;
     // exchange k: both send 16 bytes to the peer's slot k % 4 and wait for
     // the peer's; a slot is rewritten only after both passed exchange k + 3
     uint32_t xk = 0;
@@ -188,20 +199,26 @@ __global__ void __launch_bounds__(kThr + kWarp, 1)
         const uint32_t sl = xk % kXSlots, ph = (xk / kXSlots) & 1;
         ++xk;
         if (tid == 0) {
+            // release this CTA's earlier global W stores (ordered before by
+            // the CTA barrier every caller passes first) at cluster scope:
+            // the peer's TMA reads the pivot column from W after the
+            // argmax exchange
+            asm volatile("fence.acq_rel.cluster;\n" ::: "memory");
             mbar_arrive_expect_tx(&xbar[sl], 16);
             st_async16(smem_u32(&xs[sl]) + poff, a, b2, c, d, smem_u32(&xbar[sl]) + poff);
         }
         mbar_wait_cluster(&xbar[sl], ph);
         return xs[sl];
     };
-    uint32_t qrecv = 0;  // pivot columns received from the peer (qbar's phases)
+    uint32_t qk = 0;  // first-sweep chunks so far (qready's phases)
 
     uint32_t gcons = 0;
-    auto start_sweeps = [&](int passes) {
+    auto start_sweeps = [&](int passes, int side_pc) {
         fence_async_global();
         bsync();
         if (tid == 0) {
             sh.chunks = passes * nck;
+            sh.side_pc = side_pc;
             mbar_arrive(&go_bar);
         }
     };
@@ -266,7 +283,7 @@ __global__ void __launch_bounds__(kThr + kWarp, 1)
     }
 
     // ---- initial norms of own columns, max_init over both (qr.cpp:47-51) ----
-    start_sweeps(1);
+    start_sweeps(1, -1);
     double lmax = 0.0;
     {
         double s = 0.0;
@@ -380,45 +397,11 @@ __global__ void __launch_bounds__(kThr + kWarp, 1)
         }
         const int pc = sh.best_i;
         const double pn = sh.best_v;
-        // q_s = w_s / R(s,s) (qr.cpp:91-92) by the pivot's owner, into W and
-        // into both CTAs' q: plain distributed-shared stores into the peer,
-        // then ONE release-arrive on its qbar (per-element st.async would
-        // serialise 4096 transaction updates on the peer's barrier). The
-        // peer finished the previous step's sweeps before it sent this step's
-        // argmax, so its q is free.
-        if (pc >= c0 && pc < c1) {
-            // the column's strided global loads issued together, 16 per
-            // thread at a time, then divided and stored
-            for (int i0 = 0; i0 < rows; i0 += 16 * kThr) {
-                double v[16];
-#pragma unroll
-                for (int u = 0; u < 16; ++u) {
-                    const int i = i0 + u * kThr + tid;
-                    v[u] = i < rows ? W[i * npad + pc] : 0.0;
-                }
-#pragma unroll
-                for (int u = 0; u < 16; ++u) {
-                    const int i = i0 + u * kThr + tid;
-                    if (i < rows) {
-                        const double q = div_rn(v[u], pn);
-                        W[i * npad + pc] = q;
-                        qsm[i] = q;
-                        st_cluster_f64(peer_q + 8u * static_cast<uint32_t>(i), q);
-                    }
-                }
-            }
-            asm volatile("fence.acq_rel.cluster;\n" ::: "memory");
-            bsync();
-            if (tid == 0) mbar_arrive_remote(smem_u32(&qbar) + poff);
-        } else {
-            mbar_wait_cluster(&qbar, qrecv & 1);
-            ++qrecv;
-        }
         // two-pass MGS (qr.cpp:94-102) over own columns: three back-to-back
         // read sweeps (r1; r2 from w - r1 q; w'' = (w - r1 q) - r2 q stored,
         // with its norm), as cpqr.cu
         const bool act = mine && posof[j] > s;
-        start_sweeps(3);
+        start_sweeps(3, pc);
         double r1 = 0.0, r2 = 0.0, nn = 0.0;
         double* Wj = W + j;
         // rows of a chunk in order: whole groups of kGrp with the next
@@ -454,9 +437,37 @@ __global__ void __launch_bounds__(kThr + kWarp, 1)
             }
             for (int u = nfull; u < nr; ++u) f(u, qsm[i0 + u], ck[u * NH + tid]);
         };
-        sweep([&](const double* ck, int i0, int nr) {
-            if (act) rows_of(ck, i0, nr, [&](int, double q, double w) { r1 = add_rn(r1, mul_rn(q, w)); });
-        });
+        // first sweep: q_s = w_s / R(s,s) (qr.cpp:91-92), chunk by chunk, by
+        // the idle warp kQWarp of BOTH CTAs from the pivot column pair the
+        // producer loads beside each chunk (the same div_rn, so the same
+        // bits in both; no transfer between the CTAs). The column warps
+        // wait for a chunk's q before its r1 terms; sweeps 2 and 3 find all
+        // of q in qsm. CTA 0 also stores q as Q's column s (the Q output).
+        // W's pivot column is left as it is: the peer may still be reading
+        // it for this sweep.
+        double* qo = p.Qout && crank == 0 ? p.Qout + (static_cast<size_t>(b) * p.kcap + s) * rows : nullptr;
+        for (int c = 0; c < nck; ++c, ++gcons, ++qk) {
+            const uint32_t slot = gcons % kStages, qs = qk % kStages;
+            mbar_wait(&ring_full[slot], (gcons / kStages) & 1);
+            const int i0 = c * ring_rows, nr = min(ring_rows, rows - i0);
+            if (warp == kQWarp) {
+                const double* pcol = side + static_cast<size_t>(slot) * ring_rows * 2 + (pc & 1);
+                for (int u = lane; u < nr; u += kWarp) {
+                    const double q = div_rn(pcol[2 * u], pn);
+                    qsm[i0 + u] = q;
+                    if (qo) qo[i0 + u] = q;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&qready[qs]);
+            } else if (warp < NH / kWarp) {
+                mbar_wait(&qready[qs], (qk / kStages) & 1);
+                if (act)
+                    rows_of(ring + slot * (kStageBytes / sizeof(double)), i0, nr,
+                            [&](int, double q, double w) { r1 = add_rn(r1, mul_rn(q, w)); });
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ring_empty[slot]);
+        }
         sweep([&](const double* ck, int i0, int nr) {
             if (act)
                 rows_of(ck, i0, nr, [&](int, double q, double w) { r2 = add_rn(r2, mul_rn(q, sub_rn(w, mul_rn(r1, q)))); });
@@ -504,13 +515,6 @@ __global__ void __launch_bounds__(kThr + kWarp, 1)
         for (int t = 0; t < rank; ++t)
             if (fabs(diag[t]) < 1e-14 * max_diag || max_diag == 0.0) sing = 1;
         sh.flag = sing;
-    }
-    if (p.Qout && crank == 0) {
-        double* Qo = p.Qout + static_cast<size_t>(b) * rows * p.kcap;
-        for (int e = tid; e < rank * rows; e += kThr) {
-            const int i = e % rows, t = e / rows;
-            Qo[static_cast<size_t>(t) * rows + i] = W[i * npad + perm[t]];
-        }
     }
     bsync();
     if (sh.flag && rank < n) {
@@ -579,7 +583,8 @@ __global__ void __launch_bounds__(kThr + kWarp, 1)
 }
 
 template <int NH>
-cudaError_t launch_pair_t(const CpqrParams& p, const CUtensorMap* wmap, int ring_rows, cudaStream_t stream) {
+cudaError_t launch_pair_t(const CpqrParams& p, const CUtensorMap* wmap, const CUtensorMap* pmap, int ring_rows,
+                          cudaStream_t stream) {
     auto kern = cpqr_pair_kernel<NH>;
     const size_t smem = cpqr_pair_smem_bytes(p.rows, p.n, p.step_cap);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -596,13 +601,15 @@ cudaError_t launch_pair_t(const CpqrParams& p, const CUtensorMap* wmap, int ring
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, p, *wmap, ring_rows);
+    return cudaLaunchKernelEx(&cfg, kern, p, *wmap, *pmap, ring_rows);
 }
 
 }  // namespace
 
 size_t cpqr_pair_smem_bytes(int64_t rows, int64_t n, int64_t step_cap) {
-    return 128 + static_cast<size_t>(kStages) * kStageBytes + sizeof(double) * ((rows + 1) & ~int64_t(1)) +
+    return 128 + static_cast<size_t>(kStages) * kStageBytes +
+           static_cast<size_t>(kStages) * cpqr_pair_ring_rows(n) * 2 * sizeof(double) +
+           sizeof(double) * ((rows + 1) & ~int64_t(1)) +
            sizeof(double) * n + 2 * sizeof(int) * n + 16 + sizeof(double) * step_cap;
 }
 
@@ -618,12 +625,13 @@ int cpqr_pair_ring_rows(int64_t n) {
     return r > 256 ? 256 : r;
 }
 
-cudaError_t launch_cpqr_pair(const CpqrParams& p, const CUtensorMap* wmap, cudaStream_t stream) {
+cudaError_t launch_cpqr_pair(const CpqrParams& p, const CUtensorMap* wmap, const CUtensorMap* pmap,
+                             cudaStream_t stream) {
     if (!cpqr_pair_supported(p.rows, p.n, p.mode, p.step_cap) || p.npad != 2 * cpqr_pair_half(p.n))
         return cudaErrorInvalidValue;
     const int rr = cpqr_pair_ring_rows(p.n);
-    return cpqr_pair_half(p.n) == 128 ? launch_pair_t<128>(p, wmap, rr, stream)
-                                      : launch_pair_t<64>(p, wmap, rr, stream);
+    return cpqr_pair_half(p.n) == 128 ? launch_pair_t<128>(p, wmap, pmap, rr, stream)
+                                      : launch_pair_t<64>(p, wmap, pmap, rr, stream);
 }
 
 }  // namespace spidgpu

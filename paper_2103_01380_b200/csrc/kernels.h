@@ -48,13 +48,15 @@ int cpqr_tall_ring_rows(int64_t n);
 cudaError_t launch_cpqr_tall(const CpqrParams& p, const CUtensorMap* wmap, cudaStream_t stream);
 // tall inputs with 64 < n <= 256 and the fixed / tolerance rules: each
 // subdomain's columns split over a cluster of two CTAs (cpqr_pair.cu); W rows
-// are 2 * cpqr_pair_half(n) long, the TMA box is {half, ring_rows, 1} and the
+// are 2 * cpqr_pair_half(n) long, the TMA box is {half, ring_rows, 1} (pmap: the
+// same map with box {2, ring_rows, 1}, the pivot column pair) and the
 // r11 workspace holds two step_cap^2 blocks per subdomain
 size_t cpqr_pair_smem_bytes(int64_t rows, int64_t n, int64_t step_cap);
 bool cpqr_pair_supported(int64_t rows, int64_t n, int mode, int64_t step_cap);
 int cpqr_pair_half(int64_t n);
 int cpqr_pair_ring_rows(int64_t n);
-cudaError_t launch_cpqr_pair(const CpqrParams& p, const CUtensorMap* wmap, cudaStream_t stream);
+cudaError_t launch_cpqr_pair(const CpqrParams& p, const CUtensorMap* wmap, const CUtensorMap* pmap,
+                             cudaStream_t stream);
 // register-resident variant for sketch-sized inputs (rows <= 80, n <= 512)
 bool cpqr_reg_supported(int64_t rows, int64_t n, int64_t step_cap);
 cudaError_t launch_cpqr_reg(const CpqrParams& p, cudaStream_t stream);
