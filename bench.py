@@ -806,17 +806,18 @@ def pipeline_measure(cfg, A, args):
             p.h.check(N.lib.spidgpu_archive_view(p.h.h, C.byref(view), C.byref(ln)))
             return C.string_at(view.value, ln.value), p.stats(), dt
 
-    # median of 3 timed runs per source after one warm-up: the host-frame run
-    # is a chain of 256 synchronous PCIe copies and swings with the host
+    # median of 5 timed runs per source after one warm-up: the host-frame run
+    # is a chain of 256 synchronous PCIe copies and swings with the host, and
+    # on this pool even device-frame runs see occasional multi-ms host stalls
     run(frames)
     torch.cuda.synchronize()
-    runs = sorted((run(frames) for _ in range(3)), key=lambda r: r[2])
-    data, st, s_dev = runs[1]
+    runs = sorted((run(frames) for _ in range(5)), key=lambda r: r[2])
+    data, st, s_dev = runs[2]
     host = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
     host.copy_(frames)
     hf = host.numpy()
-    runs_h = sorted((run(hf) for _ in range(3)), key=lambda r: r[2])
-    data_h, _, s_host = runs_h[1]
+    runs_h = sorted((run(hf) for _ in range(5)), key=lambda r: r[2])
+    data_h, _, s_host = runs_h[2]
     del host, runs, runs_h
     dec = torch.empty((n, m), dtype=torch.float64, device=field.device).T
     AR.decompress(data, out=dec)
