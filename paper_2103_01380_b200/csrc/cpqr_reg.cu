@@ -28,6 +28,27 @@ struct Sh {
     int best_i, stop, flag;
 };
 
+// per-warp staging of the column load: 32 columns x 16 rows, row stride 17
+// (conflict-free column reads by the owning lanes)
+constexpr int kStageRows = 16, kStagePitch = kStageRows + 1;
+constexpr size_t kStageBytes = sizeof(double) * (kT / kWarp) * kWarp * kStagePitch;
+
+// sum_{pos = lo}^{hi - 1} v[pos], left to right (a serial chain), the loads
+// issued eight at a time ahead of the adds
+__device__ __forceinline__ double sum_in_order(const double* v, int lo, int hi) {
+    double acc = 0.0;
+    int pos = lo;
+    for (; pos + 8 <= hi; pos += 8) {
+        double t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t[u] = v[pos + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = add_rn(acc, t[u]);
+    }
+    for (; pos < hi; ++pos) acc = add_rn(acc, v[pos]);
+    return acc;
+}
+
 template <int ROWS, int CPT>
 __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -42,6 +63,7 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
     const int rows = static_cast<int>(p.rows), n = static_cast<int>(p.n);
     const int cap = static_cast<int>(p.step_cap);
     // dynamic smem: nrm[n] colsq[n] diag[cap] | perm[n] posof[n] | X[cap][n] R11[cap][cap]
+    // (X and R11 double as the load's staging area before the pivot loop)
     double* nrm = reinterpret_cast<double*>(smem_raw);
     double* colsq = nrm + n;
     double* diag = colsq + n;
@@ -74,17 +96,32 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
     // compiler schedules each group's independent products ahead of its
     // dependent adds instead of branching per element
     constexpr int kGrp = 16;
+    // Loaded through a per-warp shared staging tile so that each load
+    // instruction covers two 128-byte column segments instead of 32 columns'
+    // lines (the per-thread column walk was L1-tag bound: ~7 us per launch).
     int bad = 0;
+    {
+        double* stg = X + warp * (kWarp * kStagePitch);
+        const int half = lane >> 4, r = lane & 15;
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-        const int j = tid + c * kT;
-        const double* yj = Y + static_cast<size_t>(j < n ? j : 0) * p.ldy;
+        for (int c = 0; c < CPT; ++c) {
+            const int jw = c * kT + warp * kWarp;  // this warp's first column
 #pragma unroll
-        for (int i = 0; i < ROWS; ++i) {
-            double v = 0.0;
-            if (j < n && i < rows) v = yj[i];
-            bad |= !isfinite(v);
-            w[c][i] = v;
+            for (int r0 = 0; r0 < ROWS; r0 += kStageRows) {
+#pragma unroll
+                for (int it = 0; it < kWarp / 2; ++it) {
+                    const int cl = 2 * it + half, j = jw + cl, i = r0 + r;
+                    double v = 0.0;
+                    if (j < n && i < rows) v = Y[static_cast<size_t>(j) * p.ldy + i];
+                    bad |= !isfinite(v);
+                    stg[cl * kStagePitch + r] = v;
+                }
+                __syncwarp();
+#pragma unroll
+                for (int u = 0; u < kStageRows; ++u)
+                    if (r0 + u < ROWS) w[c][r0 + u] = stg[lane * kStagePitch + u];
+                __syncwarp();
+            }
         }
     }
     for (int j = tid; j < n; j += kT) {
@@ -127,11 +164,7 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
         double m = 0.0;
         for (int k = 0; k < kT / kWarp; ++k) m = fmax(m, red_v[k]);
         sh.max_init = m;
-        if (p.mode == RULE_BLOCKED) {
-            double f = 0.0;
-            for (int j = 0; j < n; ++j) f = add_rn(f, colsq[j]);
-            sh.yfro = sqrt(f);
-        }
+        if (p.mode == RULE_BLOCKED) sh.yfro = sqrt(sum_in_order(colsq, 0, n));
     }
     __syncthreads();
     const double max_init = sh.max_init;
@@ -177,15 +210,12 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
         if (p.mode == RULE_TOL && v <= p.tol * max_init) stop = 1;  // qr.cpp:74-76
         if (p.mode == RULE_BLOCKED && s > 0 && s % p.kstep == 0) {
             // residual_fro after s steps in position order (qr.cpp:111-115):
-            // a serial sum, computed by one thread and broadcast
-            if (tid == 0) {
-                double rsq = 0.0;
-                for (int pos = s; pos < n; ++pos) {
-                    const double nj = nrm[perm[pos]];
-                    rsq = add_rn(rsq, mul_rn(nj, nj));
-                }
-                sh.flag = sqrt(rsq) <= p.tol * sh.yfro;
-            }
+            // the squares in parallel into position order, their serial sum
+            // by one thread, broadcast
+            for (int j = tid; j < n; j += kT)
+                if (posof[j] >= s) colsq[posof[j]] = mul_rn(nrm[j], nrm[j]);
+            __syncthreads();
+            if (tid == 0) sh.flag = sqrt(sum_in_order(colsq, s, n)) <= p.tol * sh.yfro;
             __syncthreads();
             if (sh.flag) stop = 1;
         }
@@ -205,6 +235,7 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
             posof[ix] = s;
             posof[cs] = ps;
             R[static_cast<size_t>(s) * n + ix] = v;  // qr.cpp:89-90
+            X[s * n + ix] = v;
             diag[s] = v;
         }
         const int pc = ix;
@@ -276,7 +307,9 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
                     w[c][i + 1] = v1;
                     nn = add_rn(nn, mul_rn(v1, v1));
                 }
-                R[static_cast<size_t>(s) * n + j] = add_rn(r1, r2);
+                const double rs = add_rn(r1, r2);
+                R[static_cast<size_t>(s) * n + j] = rs;  // global: the R output
+                X[s * n + j] = rs;                       // shared: R11 and the solve
                 nrm[j] = sqrt(nn);
             }
         }
@@ -290,12 +323,12 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
     }
 
     // ---- residual_fro (qr.cpp:111-115), singular pivots (qr.cpp:135-140) ------
+    // the squares in parallel, stored in position order; their sum in
+    // position order by one thread
+    for (int j = tid; j < n; j += kT) colsq[posof[j]] = mul_rn(nrm[j], nrm[j]);
+    __syncthreads();
     if (tid == 0) {
-        double rsq = 0.0;
-        for (int pos = rank; pos < n; ++pos) {
-            const double nj = nrm[perm[pos]];
-            rsq = add_rn(rsq, mul_rn(nj, nj));
-        }
+        const double rsq = sum_in_order(colsq, rank, n);
         p.resid[b] = sqrt(rsq);
         double max_diag = 0.0;
         for (int t = 0; t < rank; ++t) max_diag = fmax(max_diag, fabs(diag[t]));
@@ -311,13 +344,11 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
     }
 
     // ---- coefficients (id.cpp:9-28, back substitution qr.cpp:143-149) ---------
+    // R(s, col) is in X[s][col] since the pivot loop
     for (int e = tid; e < rank * rank; e += kT) {
         const int ii = e / rank, jj = e % rank;
-        r11[e] = jj >= ii ? R[static_cast<size_t>(ii) * n + perm[jj]] : 0.0;
+        r11[e] = jj >= ii ? X[ii * n + perm[jj]] : 0.0;
     }
-    for (int j = tid; j < n; j += kT)
-        if (posof[j] >= rank)
-            for (int t = 0; t < rank; ++t) X[t * n + j] = R[static_cast<size_t>(t) * n + j];
     __syncthreads();
     double* C = p.C + static_cast<size_t>(b) * p.strideC;
     const int kcap = static_cast<int>(p.kcap);
@@ -363,8 +394,8 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
 }
 
 size_t reg_smem(int64_t n, int64_t cap) {
-    return sizeof(double) * (2 * n + cap) + sizeof(int) * 2 * n + 16 +
-           sizeof(double) * (cap * n + cap * cap);
+    const size_t xr = sizeof(double) * (cap * n + cap * cap);
+    return sizeof(double) * (2 * n + cap) + sizeof(int) * 2 * n + 16 + (xr > kStageBytes ? xr : kStageBytes);
 }
 
 template <int ROWS, int CPT>
