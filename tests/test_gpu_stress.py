@@ -85,14 +85,27 @@ def test_compress_verify_repeats_bitwise_and_in_bounds(engine, field):
     assert _guards_intact(bs) and _guards_intact(bc) and _guards_intact(bi)
 
 
-def test_tall_cpqr_repeats_bitwise(engine):
+@pytest.mark.parametrize("S,n,rows", [(16, 256, 4096), (64, 130, 2500), (64, 200, 1000)])
+def test_tall_cpqr_repeats_bitwise(engine, S, n, rows):
     """The TMA-ring column ID (rows >= 256): W streamed through shared memory
-    by a producer warp, 5 repeats bitwise identical."""
+    by a producer warp; by default over CTA pairs (argmax exchange, the pivot
+    column loaded and divided in both CTAs). 5 repeats with pairs on, then 2
+    with pairs off (the single-CTA kernel), all bitwise identical."""
+    from paper_2103_01380_b200 import _native as N
     from paper_2103_01380_b200.spid import RankRule
 
-    torch.manual_seed(4)
-    Y = torch.randn((16, 256, 4096), dtype=torch.float64, device="cuda")
-    ref = engine.cpqr(Y, RankRule.fixed(32))
-    for _ in range(5):
-        out = engine.cpqr(Y, RankRule.fixed(32))
-        assert torch.equal(out.indices, ref.indices) and torch.equal(out.coeffs, ref.coeffs)
+    torch.manual_seed(4 + n)
+    Y = torch.randn((S, n, rows), dtype=torch.float64, device="cuda")
+    rule = RankRule.fixed(32)
+    ref, *ref_qr = engine.cpqr(Y, rule, want_qr=True)
+    runs = [1] * 5 + [0] * 2
+    try:
+        for pairs in runs:
+            engine.h.check(N.lib.spidgpu_set_option(engine.h.h, N.SPIDGPU_OPT_TALL_PAIRS, pairs))
+            out, *qr = engine.cpqr(Y, rule, want_qr=True)
+            for f in ("indices", "coeffs", "rank", "residual_fro", "status"):
+                assert torch.equal(getattr(out, f), getattr(ref, f)), (pairs, f)
+            for a, b in zip(qr, ref_qr):  # pivots, R, Q
+                assert torch.equal(a, b), pairs
+    finally:
+        engine.h.check(N.lib.spidgpu_set_option(engine.h.h, N.SPIDGPU_OPT_TALL_PAIRS, 1))
