@@ -65,21 +65,13 @@ __device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t peer) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(peer));
     return r;
 }
-// 16 / 8 bytes into the peer's shared memory, completing on its mbarrier
+// 16 bytes into the peer's shared memory, completing on its mbarrier
 __device__ __forceinline__ void st_async16(uint32_t raddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
                                            uint32_t rbar) {
     asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];\n" ::"r"(
                      raddr),
                  "r"(a), "r"(b), "r"(c), "r"(d), "r"(rbar)
                  : "memory");
-}
-__device__ __forceinline__ void st_cluster_f64(uint32_t raddr, double v) {
-    asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(raddr), "d"(v) : "memory");
-}
-// arrive on the peer's mbarrier, releasing this thread's prior writes (and,
-// after a CTA barrier, the CTA's) at cluster scope
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t rbar) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(rbar) : "memory");
 }
 // wait with cluster-scope acquire (the data came from the peer by st.async)
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
