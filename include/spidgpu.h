@@ -113,6 +113,12 @@ int64_t spidgpu_launch_count(spidgpu_handle h);
  * cluster of two CTAs (1, default) or on one CTA (0); bitwise the same
  * factors (tests and A/B). */
 #define SPIDGPU_OPT_TALL_PAIRS 7
+/* SPIDGPU_OPT_REG_PAIRS = 8: sketch-sized column IDs with 33-48 rows,
+ * 128 < n <= 256 columns, the fixed or tolerance rule and at most one pair
+ * per two SMs (config 3's 48 x 256 sketches) run each subdomain's columns on
+ * a cluster of two CTAs (1, default) or on one CTA (0); bitwise the same
+ * factors (tests and A/B). */
+#define SPIDGPU_OPT_REG_PAIRS 8
 int spidgpu_set_option(spidgpu_handle h, int option, int64_t value);
 /* Instrumentation: out[0..2] = tcgen05-sketch converter-warp flushes since
  * the last reset, by cause (segment end, exponent-headroom overflow,

@@ -25,6 +25,7 @@ SPIDGPU_OPT_SKETCH_SMS = 4
 SPIDGPU_OPT_SKETCH_PAIRS = 5
 SPIDGPU_OPT_SKETCH_SEG_ROWS = 6
 SPIDGPU_OPT_TALL_PAIRS = 7
+SPIDGPU_OPT_REG_PAIRS = 8
 
 
 class SpidError(RuntimeError):

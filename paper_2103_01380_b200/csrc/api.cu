@@ -217,7 +217,12 @@ int do_cpqr(spidgpu_handle h, Workspace& ws, const double* Y, int64_t rows, int6
     p.Rout = R;
     p.Qout = Q;
     if (reg) {
-        CK(h, launch_cpqr_reg(p, st));
+        // sketch-sized inputs (33-48 rows, 128 < n <= 256): columns over a
+        // CTA pair where it measured faster (tools/exp_regpair_ab.py), i.e.
+        // while the pairs fit one wave
+        const bool rpair = h->reg_pairs && 2 * batch <= h->num_sms &&
+                           cpqr_regpair_supported(rows, n, rule->mode, step_cap);
+        CK(h, rpair ? launch_cpqr_regpair(p, st) : launch_cpqr_reg(p, st));
     } else if (tall) {
         CUtensorMap wmap;
         cuuint64_t gdim[3] = {static_cast<cuuint64_t>(npad), static_cast<cuuint64_t>(rows),
@@ -620,6 +625,7 @@ int spidgpu_set_option(spidgpu_handle h, int option, int64_t value) {
     switch (option) {
         case SPIDGPU_OPT_GENERIC_CPQR: h->force_generic_cpqr = value != 0; return SPID_OK;
         case SPIDGPU_OPT_TALL_PAIRS: h->tall_pairs = value != 0; return SPID_OK;
+        case SPIDGPU_OPT_REG_PAIRS: h->reg_pairs = value != 0; return SPID_OK;
         case SPIDGPU_OPT_DMMA_SKETCH: h->force_dmma_sketch = value != 0; return SPID_OK;
         case SPIDGPU_OPT_SKETCH_PAIRS:
             if (value < 0 || value > 2) return SPID_INVALID_ARGUMENT;

@@ -87,6 +87,7 @@ struct spidgpu_context {
     int sketch_sms = 0;               // SMs the persistent sketch grid may occupy (0 = all)
     int sketch_pairs = 1;             // tcgen05 sketch CTA pairs: 0/1 off (ell <= 64), 2 always, 3 split (80)
     bool tall_pairs = true;           // tall column IDs with 64 < n <= 256 over a cluster of two
+    bool reg_pairs = true;            // sketch-sized column IDs with 128 < n <= 256 over a cluster of two
     int64_t sketch_seg_rows = 0;      // tcgen05 sketch segment rows (0 = kSketchSegRows; experiments)
     uint8_t* archive_pinned = nullptr;  // last archive built by spidgpu_archive_compress
     size_t archive_cap = 0, archive_size = 0;

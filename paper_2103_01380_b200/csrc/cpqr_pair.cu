@@ -26,12 +26,15 @@
 // the single-CTA kernel.
 #include <math.h>
 
+#include "cluster.cuh"
 #include "common.cuh"
 #include "kernels.h"
 
 namespace spidgpu {
 
 namespace {
+
+using namespace cluster;
 
 constexpr int kThr = 256;                 // column threads per CTA (8 warps)
 constexpr int kProducer = kThr / kWarp;   // the 9th warp streams W
@@ -51,38 +54,6 @@ __device__ __forceinline__ int bsync_or(int v) {
         : "memory");
     return r;
 }
-__device__ __forceinline__ uint32_t ctarank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-    return r;
-}
-// all threads of both CTAs (the producer warps included: they arrive too)
-__device__ __forceinline__ void cluster_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-__device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t peer) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(peer));
-    return r;
-}
-// 16 bytes into the peer's shared memory, completing on its mbarrier
-__device__ __forceinline__ void st_async16(uint32_t raddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
-                                           uint32_t rbar) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];\n" ::"r"(
-                     raddr),
-                 "r"(a), "r"(b), "r"(c), "r"(d), "r"(rbar)
-                 : "memory");
-}
-// wait with cluster-scope acquire (the data came from the peer by st.async)
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
-    asm volatile(
-        "{\n.reg .pred p;\nWAITC_%=:\n"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAITC_%=;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-
 struct PairShared {
     double best_v, max_init;
     int best_i, stop, flag, chunks, side_pc;

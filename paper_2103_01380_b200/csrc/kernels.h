@@ -57,6 +57,11 @@ int cpqr_pair_half(int64_t n);
 int cpqr_pair_ring_rows(int64_t n);
 cudaError_t launch_cpqr_pair(const CpqrParams& p, const CUtensorMap* wmap, const CUtensorMap* pmap,
                              cudaStream_t stream);
+// the register-resident column ID with each subdomain's columns split over a
+// cluster of two CTAs (cpqr_reg_pair.cu): 32 < rows <= 48, 128 < n <= 256,
+// fixed / tolerance rules; R in r_ws as for cpqr_reg
+bool cpqr_regpair_supported(int64_t rows, int64_t n, int mode, int64_t step_cap);
+cudaError_t launch_cpqr_regpair(const CpqrParams& p, cudaStream_t stream);
 // register-resident variant for sketch-sized inputs (rows <= 80, n <= 512)
 bool cpqr_reg_supported(int64_t rows, int64_t n, int64_t step_cap);
 cudaError_t launch_cpqr_reg(const CpqrParams& p, cudaStream_t stream);
