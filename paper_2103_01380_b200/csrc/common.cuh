@@ -146,6 +146,32 @@ __device__ __forceinline__ void warp_argmax(double& v, int& idx) {
     }
 }
 
+// The same order on integer keys, for the register CPQR whose MGS passes
+// saturate the FP64 pipe (DSETP runs there too). A candidate's norm is
+// non-negative or NaN, or -1.0 for "no live column"; for these the IEEE bit
+// pattern read as a signed 64-bit integer orders exactly like the value (-1.0
+// is negative, every norm is not), and NaN maps below everything: a NaN norm
+// can never beat the -1.0 start of the double comparison either, so the
+// chosen pivot is the same.
+__device__ __forceinline__ long long norm_key(double v) {
+    const long long b = __double_as_longlong(v);
+    return (b & 0x7fffffffffffffffLL) > 0x7ff0000000000000LL ? (-0x7fffffffffffffffLL - 1) : b;
+}
+__device__ __forceinline__ bool key_better_k(long long ka, int ia, long long kb, int ib) {
+    return ka > kb || (ka == kb && ia < ib);
+}
+__device__ __forceinline__ void warp_argmax_k(long long& k, int& idx) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const long long ok = __shfl_xor_sync(0xffffffffu, k, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, idx, off);
+        if (key_better_k(ok, oi, k, idx)) {
+            k = ok;
+            idx = oi;
+        }
+    }
+}
+
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));

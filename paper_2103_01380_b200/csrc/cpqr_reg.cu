@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ Sh sh;
     __shared__ double red_v[kT / kWarp];
+    __shared__ long long red_k[kT / kWarp];
     __shared__ int red_i[kT / kWarp];
     __shared__ __align__(16) double qbuf[ROWS + 2];
     const double2* q2 = reinterpret_cast<const double2*>(qbuf);
@@ -180,32 +181,37 @@ __global__ void __launch_bounds__(kT, 1) cpqr_reg_kernel(CpqrParams p) {
 #pragma unroll
     for (int c = 0; c < CPT; ++c) alive[c] = tid + c * kT < n;
     for (int s = 0; s < step_limit; ++s) {
-        double bv = -1.0;
+        // integer keys (norm_key): the argmax stays off the FP64 pipe
+        long long bk = norm_key(-1.0);
         int bi = 0x7fffffff;
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
             const int j = tid + c * kT;
-            if (alive[c] && key_better(nrm[j], j, bv, bi)) {
-                bv = nrm[j];
-                bi = j;
+            if (alive[c]) {
+                const long long kj = norm_key(nrm[j]);
+                if (key_better_k(kj, j, bk, bi)) {
+                    bk = kj;
+                    bi = j;
+                }
             }
         }
-        warp_argmax(bv, bi);
+        warp_argmax_k(bk, bi);
         if (lane == 0) {
-            red_v[warp] = bv;
+            red_k[warp] = bk;
             red_i[warp] = bi;
         }
         __syncthreads();
         // every thread reduces the 8 warp partials in the same order (a total
         // order, so the same winner); no serial section, no broadcast barrier
-        double v = red_v[0];
+        long long vk = red_k[0];
         int ix = red_i[0];
 #pragma unroll
         for (int k = 1; k < kT / kWarp; ++k)
-            if (key_better(red_v[k], red_i[k], v, ix)) {
-                v = red_v[k];
+            if (key_better_k(red_k[k], red_i[k], vk, ix)) {
+                vk = red_k[k];
                 ix = red_i[k];
             }
+        const double v = __longlong_as_double(vk);
         int stop = 0;
         if (p.mode == RULE_TOL && v <= p.tol * max_init) stop = 1;  // qr.cpp:74-76
         if (p.mode == RULE_BLOCKED && s > 0 && s % p.kstep == 0) {

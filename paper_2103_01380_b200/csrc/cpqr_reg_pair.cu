@@ -63,6 +63,7 @@ template <int ROWS>
 __global__ void __launch_bounds__(kT, 1) cpqr_regpair_kernel(CpqrParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ double red_v[kT / kWarp];
+    __shared__ long long red_k[kT / kWarp];
     __shared__ int red_i[kT / kWarp];
     __shared__ __align__(16) double qbuf[ROWS + 2];     // q_s, divided
     __shared__ __align__(16) double qloc[ROWS];         // this CTA's best candidate column
@@ -202,26 +203,31 @@ __global__ void __launch_bounds__(kT, 1) cpqr_regpair_kernel(CpqrParams p) {
     const int step_limit = static_cast<int>(p.step_limit);
     bool alive = mine;  // column not yet selected, kept in a register
     for (int s = 0; s < step_limit; ++s) {
-        double bv = -1.0;
+        // integer keys (norm_key): the argmax stays off the FP64 pipe
+        long long bk = norm_key(-1.0);
         int bi = 0x7fffffff;
         if (alive) {
-            bv = nrm[j];
-            bi = j;
+            const long long kj = norm_key(nrm[j]);
+            if (key_better_k(kj, j, bk, bi)) {
+                bk = kj;
+                bi = j;
+            }
         }
-        warp_argmax(bv, bi);
+        warp_argmax_k(bk, bi);
         if (lane == 0) {
-            red_v[warp] = bv;
+            red_k[warp] = bk;
             red_i[warp] = bi;
         }
         __syncthreads();
-        double v = red_v[0];
+        long long vk = red_k[0];
         int ix = red_i[0];
 #pragma unroll
         for (int k = 1; k < kT / kWarp; ++k)
-            if (key_better(red_v[k], red_i[k], v, ix)) {
-                v = red_v[k];
+            if (key_better_k(red_k[k], red_i[k], vk, ix)) {
+                vk = red_k[k];
                 ix = red_i[k];
             }
+        double v = __longlong_as_double(vk);
         // the exchange: (norm, index) and the candidate column into the
         // peer's slot and its qrem[s & 1] (a CTA with no live column sends
         // zeros); the peer cannot run two steps ahead of this CTA's reads of
