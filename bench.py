@@ -797,15 +797,18 @@ def pipeline_measure(cfg, A, args):
 
     from paper_2103_01380_b200 import _native as N
 
-    def run(src):
+    def run(src, sync=False):
         """push every frame + spidgpu_stream_finish (the archive lands in the
         handle's pinned buffer) -- timed; the copy into a Python bytes object
         (first-touch page faults of 60 MB, ~27 ms) is not the library's work
-        and happens after the clock stops"""
+        and happens after the clock stops. Device frames are always read
+        asynchronously; host frames with sync=False too (they stay resident
+        and unmodified until finish, so the copies queue back to back), with
+        sync=True every push waits for its frame's copy"""
         with PL.Pipeline(pc) as p:
             t = time.perf_counter()
             for j in range(n):
-                p.push(src[j])
+                p.push(src[j], sync=sync)
             nb = C.c_int64()
             p._check(N.lib.spidgpu_stream_finish(p.s, C.byref(nb)))
             torch.cuda.synchronize()
@@ -826,6 +829,8 @@ def pipeline_measure(cfg, A, args):
     hf = host.numpy()
     runs_h = sorted((run(hf) for _ in range(5)), key=lambda r: r[2])
     data_h, _, s_host = runs_h[2]
+    # synchronous host pushes (each waits for its own frame's copy), for comparison
+    data_hs, _, s_host_sync = sorted((run(hf, True) for _ in range(3)), key=lambda r: r[2])[1]
     del host, runs, runs_h
     dec = torch.empty((n, m), dtype=torch.float64, device=field.device).T
     AR.decompress(data, out=dec)
@@ -838,10 +843,13 @@ def pipeline_measure(cfg, A, args):
                              "snapshots_per_s": n / s_dev},
            "e2e": {"value": raw / s_host / 1e9, "unit": "GB/s", "ms": s_host * 1e3,
                    "h2d_bytes_per_step": raw, "d2h_bytes_per_step": len(data_h),
-                   "api": "spidgpu_stream_push per snapshot from pinned host memory + spidgpu_stream_finish "
-                          "(archive D2H into the handle's pinned buffer; the Python bytes copy is untimed)"},
+                   "sync_push": {"value": raw / s_host_sync / 1e9, "ms": s_host_sync * 1e3},
+                   "api": "spidgpu_stream_push per snapshot from pinned host memory (asynchronous pushes: the "
+                          "frames stay unmodified until finish; sync_push = each push waits for its frame's "
+                          "copy) + spidgpu_stream_finish (archive D2H into the handle's pinned buffer; the "
+                          "Python bytes copy is untimed)"},
            "stage1_ms": st["stage1_ms"], "stage2_ms": st["stage2_ms"],
-           "host_and_device_identical": data == data_h}
+           "host_and_device_identical": data == data_h and data == data_hs}
     try:
         import oracle
         ref = oracle.ref()

@@ -474,8 +474,12 @@ typedef struct spidgpu_overlap {  /* spid::OverlapReport, pipeline.hpp:52-56 */
 int spidgpu_stream_open(spidgpu_handle h, const spidgpu_stream_config* cfg,
                         spidgpu_stream_handle* out);
 /* Push `count` snapshots (m x count, ld ld; m must equal the grid's point
- * count, else GeometryMismatch). on_device != 0: `frames` is a device pointer
- * that may be reused when the call returns. */
+ * count, else GeometryMismatch). on_device: 0 host frames, read (copied)
+ * before the call returns, so the caller may reuse them then; 1 device
+ * frames, 2 host frames (pinned, for an asynchronous copy): read
+ * asynchronously in push order, so the caller keeps them unmodified until
+ * spidgpu_stream_finish returns, and consecutive host pushes queue their
+ * copies back to back instead of waiting for each other. */
 int spidgpu_stream_push(spidgpu_stream_handle s, const double* frames, int64_t m, int64_t count,
                         int64_t ld, int32_t on_device);
 /* Close the final short chunks, run stage 2, emit the archive into the parent

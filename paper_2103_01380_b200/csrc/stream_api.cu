@@ -83,6 +83,9 @@ struct spidgpu_stream {
     DevBuf staging[2];
     int64_t staged[2] = {0, 0};  // entries each staging buffer holds
     cudaEvent_t copied = nullptr;
+    cudaStream_t s_copy = nullptr;           // host frames' copies into staging
+    cudaEvent_t stg_free[2] = {nullptr, nullptr};  // the gather that last read staging[i] is done
+    bool stg_used[2] = {false, false};
     int stg = 0;
     int64_t filled = 0, snapshots = 0, nchunks = 0, stage1_tasks = 0, stage2_tasks = 0;
     int64_t fine_peak = 0, coarse_peak = 0;
@@ -198,6 +201,7 @@ void destroy(spidgpu_stream* s) {
     for (cudaStream_t st : s->s_lane)
         if (st) cudaStreamSynchronize(st);
     if (s->s_in) cudaStreamSynchronize(s->s_in);
+    if (s->s_copy) cudaStreamSynchronize(s->s_copy);
     for (SGroup& g : s->groups) {
         for (ChunkArena& c : g.chunks)
             if (c.mem) cudaFree(c.mem);
@@ -211,6 +215,8 @@ void destroy(spidgpu_stream* s) {
     s->staging[0].release();
     s->staging[1].release();
     if (s->copied) cudaEventDestroy(s->copied);
+    for (cudaEvent_t e : s->stg_free)
+        if (e) cudaEventDestroy(e);
     for (auto& e : s->s1_events) {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
@@ -226,6 +232,7 @@ void destroy(spidgpu_stream* s) {
     for (cudaEvent_t e : s->free_ev)
         if (e) cudaEventDestroy(e);
     if (s->s_in) cudaStreamDestroy(s->s_in);
+    if (s->s_copy) cudaStreamDestroy(s->s_copy);
     for (cudaStream_t st : s->s_lane)
         if (st) cudaStreamDestroy(st);
 }
@@ -274,6 +281,9 @@ int spidgpu_stream_open(spidgpu_handle h, const spidgpu_stream_config* cfg, spid
         lanes_ok = lanes_ok && cudaStreamCreateWithFlags(&s->s_lane[l], cudaStreamNonBlocking) == cudaSuccess &&
                    cudaEventCreateWithFlags(&s->free_ev[l], cudaEventDisableTiming) == cudaSuccess;
     if (!lanes_ok || cudaStreamCreateWithFlags(&s->s_in, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&s->s_copy, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->stg_free[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->stg_free[1], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&s->ready, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&s->copied, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreate(&s->t0) != cudaSuccess || cudaEventRecord(s->t0, s->s_in) != cudaSuccess)
@@ -314,6 +324,11 @@ int spidgpu_stream_push(spidgpu_stream_handle s, const double* frames, int64_t m
     if (m != s->L.points)  // pipeline.cpp:116-117
         return sfail(s, SPID_GEOMETRY_MISMATCH, "producer frame size does not match grid");
     if (count > 0 && ld < m) return sfail(s, SPID_INVALID_ARGUMENT, "ld < m");
+    if (on_device < 0 || on_device > 2) return sfail(s, SPID_INVALID_ARGUMENT, "on_device must be 0, 1 or 2");
+    // 0: host frames, read before the call returns; 1: device frames, 2: host
+    // frames, both read asynchronously (the caller keeps them unmodified
+    // until finish)
+    const bool dev = on_device == 1, async = on_device != 0;
     cudaSetDevice(s->h->device);
     const int64_t T = s->cfg.time_chunk;
     Stream_push_log log(s, count);
@@ -321,14 +336,33 @@ int spidgpu_stream_push(spidgpu_stream_handle s, const double* frames, int64_t m
         const int64_t c = std::min(count - j, T - s->filled);
         const double* src = frames + j * ld;
         int64_t lds = ld;
-        if (!on_device) {  // stage the frames (the only fine-grid data the stream holds)
-            DevBuf& sb = s->staging[s->stg];
-            s->staged[s->stg] = m * c;
+        const int bi = s->stg;
+        if (!dev) {  // stage the frames (the only fine-grid data the stream holds)
+            DevBuf& sb = s->staging[bi];
+            const size_t need = sizeof(double) * m * c;
+            s->staged[bi] = m * c;
             s->stg ^= 1;
-            SCK(s, sb.ensure(sizeof(double) * m * c, s->s_in));
-            SCK(s, cudaMemcpy2DAsync(sb.ptr, sizeof(double) * m, src, sizeof(double) * ld,
-                                     sizeof(double) * m, c, cudaMemcpyHostToDevice, s->s_in));
-            SCK(s, cudaEventRecord(s->copied, s->s_in));
+            if (sb.bytes < need) {  // reallocation: no reader or writer left
+                SCK(s, cudaStreamSynchronize(s->s_copy));
+                SCK(s, cudaStreamSynchronize(s->s_in));
+            }
+            SCK(s, sb.ensure(need, s->s_in));
+            if (async) {
+                // on their own copy stream, so that a frame's copy does not
+                // queue behind the previous frame's gather; a staging buffer
+                // is rewritten only after the gather that read it
+                if (s->stg_used[bi]) SCK(s, cudaStreamWaitEvent(s->s_copy, s->stg_free[bi], 0));
+                SCK(s, cudaMemcpy2DAsync(sb.ptr, sizeof(double) * m, src, sizeof(double) * ld,
+                                         sizeof(double) * m, c, cudaMemcpyHostToDevice, s->s_copy));
+                SCK(s, cudaEventRecord(s->copied, s->s_copy));
+                SCK(s, cudaStreamWaitEvent(s->s_in, s->copied, 0));
+            } else {
+                // the host waits for this copy anyway: in stream order on s_in
+                // (measured faster than the cross-stream hand-off per frame)
+                SCK(s, cudaMemcpy2DAsync(sb.ptr, sizeof(double) * m, src, sizeof(double) * ld,
+                                         sizeof(double) * m, c, cudaMemcpyHostToDevice, s->s_in));
+                SCK(s, cudaEventRecord(s->copied, s->s_in));
+            }
             src = sb.as<double>();
             lds = m;
             s->fine_peak = std::max(s->fine_peak, s->staged[0] + s->staged[1]);
@@ -341,6 +375,10 @@ int spidgpu_stream_push(spidgpu_stream_handle s, const double* frames, int64_t m
                                             B, g.Pc, g.Pc * T, s->s_in));
             s->h->launches += 1;
         }
+        if (!dev) {
+            SCK(s, cudaEventRecord(s->stg_free[bi], s->s_in));
+            s->stg_used[bi] = true;
+        }
         s->filled += c;
         s->snapshots += c;
         j += c;
@@ -349,7 +387,7 @@ int spidgpu_stream_push(spidgpu_stream_handle s, const double* frames, int64_t m
             if (rc) return rc;
         }
     }
-    if (!on_device) SCK(s, cudaEventSynchronize(s->copied));  // the host frames have been read
+    if (!async) SCK(s, cudaEventSynchronize(s->copied));  // the host frames have been read
     return SPID_OK;
 }
 

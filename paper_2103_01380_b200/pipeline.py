@@ -91,9 +91,14 @@ class Pipeline:
         if rc:
             raise SpidError(N.status_name(rc), N.lib.spidgpu_stream_last_error(self.s).decode())
 
-    def push(self, frames):
-        """Push one frame (m,) or a block of frames (m, count): numpy (host,
-        copied inside the call) or a CUDA tensor in column-major layout."""
+    def push(self, frames, *, sync: bool = True):
+        """Push one frame (m,) or a block of frames (m, count): numpy (host)
+        or a CUDA tensor in column-major layout. CUDA frames are read
+        asynchronously: keep them unmodified until finish(). Host frames:
+        sync=True copies them before the call returns; sync=False reads them
+        asynchronously too (keep them alive and unmodified until finish();
+        pinned memory, e.g. a pinned torch tensor's .numpy(), lets the copies
+        overlap)."""
         if hasattr(frames, "is_cuda") and frames.is_cuda:
             f = frames if frames.dim() == 2 else frames.reshape(-1, 1)
             if f.shape[1] > 1 and f.stride(0) != 1:
@@ -106,7 +111,9 @@ class Pipeline:
         if f.ndim == 1:
             f = f.reshape(-1, 1, order="F")
         m, cnt = f.shape
-        self._check(N.lib.spidgpu_stream_push(self.s, C.c_void_p(f.ctypes.data), m, cnt, max(m, 1), 0))
+        if not sync and not (isinstance(frames, np.ndarray) and np.may_share_memory(f, frames)):
+            raise ValueError("sync=False needs host frames the stream can read in place (float64, column-major)")
+        self._check(N.lib.spidgpu_stream_push(self.s, C.c_void_p(f.ctypes.data), m, cnt, max(m, 1), 0 if sync else 2))
 
     def finish(self) -> bytes:
         nb = C.c_int64()

@@ -186,3 +186,30 @@ def test_event_log_causality_and_counts(PL):
     with pytest.raises(PL.SpidError) as e:
         PL.overlap_report([])
     assert e.value.name == "EmptyLog"
+
+
+def test_async_pushes_byte_identical():
+    """Host frames pushed synchronously (on_device 0) and asynchronously from
+    pinned memory (2: read in push order after the call returns, kept
+    unmodified until finish), and device frames (1), give one archive."""
+    import torch
+
+    from paper_2103_01380_b200 import pipeline as PL
+
+    g, T = 24, 5
+    cfg = PL.StreamConfig(dims=(g, g, g), blocks=(2, 2, 2), strides=(2, 2, 2), time_chunk=T, stage1_rank=3,
+                          stage2_tol=1e-6, periodic=(1, 1, 1), qoi="u", provenance="t")
+    torch.manual_seed(3)
+    n = 23
+    x = torch.linspace(0, 6.283185307179586, g, dtype=torch.float64)
+    base = (torch.sin(x)[:, None, None] * torch.cos(x)[None, :, None] * torch.cos(x)[None, None, :]).reshape(-1)
+    frames = torch.stack([base * (0.9 ** t) + 1e-3 * torch.randn(base.shape, dtype=torch.float64)
+                          for t in range(n)])  # [n, m]
+    out = {}
+    for name, src, sync in (("host", frames.numpy(), True), ("dev", frames.cuda(), True),
+                            ("host_async", frames.pin_memory().numpy(), False)):
+        with PL.Pipeline(cfg) as p:
+            for j in range(n):
+                p.push(src[j], sync=sync)
+            out[name] = p.finish()
+    assert out["host"] == out["dev"] == out["host_async"]
